@@ -1,0 +1,139 @@
+/* chase.h -- C ABI of the B200-native ChASE library (libchase_b200.so).
+ *
+ * Problem (§2; Alg. 1 Require/Ensure): for a Hermitian
+ * H (N x N, complex double), find the nev lowest ("extreme", ledger #17) eigenpairs
+ * H y = lambda y by Chebyshev-filtered subspace iteration with search space nev+nex.
+ *
+ * Data layout (§3.2):
+ *   - Ranks form an r x c grid, rank = i + j*r (column-major numbering).
+ *   - Rows of H are split into r blocks, columns into c blocks; the first (N mod r) row blocks
+ *     (resp. (N mod c) column blocks) get one extra row (ledger #19).  Rank (i,j) owns the shard
+ *     H_ij = H[row0_i : row0_i+p_i, col0_j : col0_j+q_j], column-major, leading dim ldh >= p_i,
+ *     complex double interleaved (re, im) == torch.complex128, ON THE DEVICE.
+ *   - "V-layout" blocks are q_j x ncols, rows [col0_j, col0_j+q_j), replicated over
+ *     the column communicator j.  "W-layout" blocks are p_i x ncols, rows
+ *     [row0_i, row0_i+p_i), replicated over the row communicator i.
+ *
+ * Ownership: the caller owns H and every buffer passed in; the library never frees them.  The
+ * library owns its workspace (allocated in chase_init, sized from N, nev_max+nex_max)
+ * and its CUDA stream/events and NCCL communicators.
+ *
+ * Collectives: chase_init, chase_solve, chase_filter, chase_hemm_step, chase_lanczos,
+ * chase_finalize must be called by all r*c ranks with identical scalar arguments.  Arguments are
+ * validated collectively (allreduce of an error flag) so every rank returns the same status.
+ * chase_set_option must be called identically on all ranks; chase_local_layout and
+ * chase_last_error are local.
+ *
+ * Errors: every call returns a chase_status; the message of the last failure is available from
+ * chase_last_error.  CUDA/NCCL errors leave the handle unusable (finalize it).
+ * All calls are synchronous with respect to the host (they synchronize the library stream
+ * before returning), except where stated.
+ */
+#ifndef CHASE_B200_H
+#define CHASE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct chase_handle chase_handle;
+
+typedef enum {
+  CHASE_OK = 0,
+  CHASE_E_USAGE = 2,    /* invalid arguments (S:596 exit code 2) */
+  CHASE_E_NUMERIC = 3,  /* Lanczos breakdown, CholQR failure after fallback, Jacobi non-convergence */
+  CHASE_E_IO = 4,
+  CHASE_E_CUDA = 5,
+  CHASE_E_NCCL = 6,
+  CHASE_E_NOMEM = 7,    /* workspace does not fit (memory check) */
+  CHASE_E_MAXITER = 8   /* max_iter reached; `locked` pairs in the report are valid */
+} chase_status;
+
+typedef enum { CHASE_C128 = 0 /* complex<double>, interleaved */, CHASE_C64 = 1 /* reserved */ } chase_dtype;
+
+typedef struct {
+  chase_dtype dtype;              /* only CHASE_C128 is implemented */
+  int64_t N;                      /* matrix order */
+  int32_t nev_max, nex_max;       /* workspace sizing */
+  int32_t grid_rows, grid_cols;   /* r, c; 0,0 = 1 x world.  world_size == 1 with r*c > 1 selects
+                                     the emulated-grid mode: the handle owns shard `rank` of an
+                                     r x c grid and all cross-rank sums are skipped (each call
+                                     returns this rank's partial) -- for single-GPU testing. */
+  int32_t rank, world_size;       /* rank = i + j*r */
+  const void* nccl_unique_id;     /* 128-byte ncclUniqueId, identical on all ranks; NULL if world_size == 1 */
+  int32_t cuda_device;
+  void* cuda_stream;              /* cudaStream_t to order against (e.g. torch's current stream); may be NULL */
+} chase_init_args;
+
+typedef struct {
+  int32_t iterations, locked;
+  int64_t matvecs;                /* sum over filter calls of sum_a m_a (P:729-731 footnote) */
+  double filter_flops;            /* 8 N^2 matvecs (complex) */
+  double t_all, t_lanczos, t_filter, t_qr, t_rr, t_resid;   /* seconds, Table 2 columns P:646-655 */
+  double b_sup, mu_1, mu_ne, nu, max_resid;
+} chase_report;
+
+/* Create a handle: selects the device, builds the r x c grid and NCCL world/row/col
+ * communicators (row comm: color i, key j; column comm: color j, key i), allocates workspace. */
+chase_status chase_init(chase_handle** out, const chase_init_args* args);
+
+/* Options (defaults): deg_max=36, max_iter=100, lanczos_steps=25, lanczos_runs=4, seed_v=2,
+ * seed_lanczos=3, largest=0, approx=0 (1: ritz_vectors holds an initial V-hat on entry). */
+chase_status chase_set_option(chase_handle* h, const char* key, double value);
+
+/* This rank's shard: rows [row0, row0+p) and columns [col0, col0+q) of H. */
+chase_status chase_local_layout(const chase_handle* h, int64_t* row0, int64_t* p, int64_t* col0,
+                                int64_t* q);
+
+/* Alg. 1.  H_shard: device, p x q, ldh >= p, read-only.  ritz_values: host, nev
+ * doubles, ascending.  ritz_vectors: device, V-layout q x (nev) with leading dim ldv >= q (if
+ * approx=1 it must hold >= nev+nex columns with the initial V-hat on entry).  report may be NULL.
+ * Returns CHASE_E_MAXITER with the locked pairs valid if max_iter is reached. */
+chase_status chase_solve(chase_handle* h, const void* H_shard, int64_t ldh, int64_t N, int32_t nev,
+                         int32_t nex, int32_t deg, double tol, double* ritz_values,
+                         void* ritz_vectors, int64_t ldv, chase_report* report);
+
+/* ---- hot-path rows exposed for parity tests and benchmarks ------------------ */
+
+/* (a2)/(a4) + (a3)/(a5): one fused distributed step of the three-term recurrence:
+ *   dir = 0 (forward,  Eq. w=av):  Y_i = alpha (H_ij X_j - gamma E_ij X_j) [+ beta Y_i on j = j*(i)],
+ *           X V-layout (q x ncols, ldx), Y W-layout (p x ncols, ldy); sum over the row comm.
+ *   dir = 1 (backward, Eq. v=aw):  Y_j = alpha (H_ij^H X_i - gamma E_ij^T X_i) [+ beta Y_j on i = i*(j)],
+ *           X W-layout, Y V-layout; sum over the column comm.
+ * E_ij is the restriction of I_N to the shard (nonzero on the global-diagonal crossing I_ij);
+ * H is never modified.  On return Y holds the full result, replicated. */
+chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H_shard, int64_t ldh,
+                             const void* X, int64_t ldx, void* Y, int64_t ldy, int32_t ncols,
+                             double alpha, double beta, double gamma);
+
+/* (a1)-(a5): V <- Filter(A, b_sup, mu_1, mu_ne, V, m) (Alg. 1 line 4).  V: device
+ * V-layout q x ncols (ldv); W: device W-layout workspace p x ncols (ldw), overwritten.
+ * degrees: host, ncols even integers >= 0 sorted ascending (Alg. 1 line 14).  Column a
+ * receives the damped scaled Chebyshev polynomial of degree m_a (ledger #1), ends in V-layout.
+ * matvecs (may be NULL) receives sum_a m_a. */
+chase_status chase_filter(chase_handle* h, const void* H_shard, int64_t ldh, void* V, int64_t ldv,
+                          void* W, int64_t ldw, int32_t ncols, const int32_t* degrees,
+                          double b_sup, double mu_1, double mu_ne, int64_t* matvecs);
+
+/* (a6): spectral bounds by repeated Lanczos + DoS (Alg. 1 line 2; ledger #14).
+ * Outputs (host): b_sup >= lambda_max estimate, mu_1, mu_ne (DoS quantile n_e/N), nu = max |Ritz|. */
+chase_status chase_lanczos(chase_handle* h, const void* H_shard, int64_t ldh, int32_t n_e,
+                           double* b_sup, double* mu_1, double* mu_ne, double* nu);
+
+/* Fill a V-layout block (q x ncols, ldv) with the counter-based start block (Philox4x32-10 keyed
+ * by (seed, global row, column, stream)). */
+chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t col0, int32_t ncols,
+                                uint64_t seed, uint32_t stream);
+
+chase_status chase_finalize(chase_handle* h);
+const char* chase_last_error(const chase_handle* h);
+
+/* Library build/version string (for diagnostics). */
+const char* chase_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHASE_B200_H */

@@ -1,0 +1,389 @@
+// C ABI of the ChASE B200 library + the filter driver.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include "handle.h"
+#include "rng.cuh"
+
+using namespace chase;
+
+namespace chase {
+
+// ------------------------------------------------------------------------------ collectives
+void allreduce_block(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows,
+                     int64_t ld, int ncols) {
+  if (comm_size <= 1 || !comm || ncols <= 0 || rows <= 0) return;   // !comm: emulated grid
+  if (ld == rows) {
+    CHASE_NCCL(ncclAllReduce(Y, Y, (size_t)(2 * rows * ncols), ncclDouble, ncclSum, comm, h->stream));
+    return;
+  }
+  CHASE_NCCL(ncclGroupStart());
+  for (int c = 0; c < ncols; ++c) {
+    double2* col = reinterpret_cast<double2*>(Y) + (int64_t)c * ld;
+    CHASE_NCCL(ncclAllReduce(col, col, (size_t)(2 * rows), ncclDouble, ncclSum, comm, h->stream));
+  }
+  CHASE_NCCL(ncclGroupEnd());
+}
+
+void allreduce_doubles(chase_handle* h, ncclComm_t comm, int comm_size, double* x, size_t n) {
+  if (comm_size <= 1 || !comm || n == 0) return;
+  CHASE_NCCL(ncclAllReduce(x, x, n, ncclDouble, ncclSum, comm, h->stream));
+}
+
+// ------------------------------------------------------------------- fused recurrence step
+void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
+               void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma) {
+  if (ncols <= 0) return;
+  const Grid& g = h->grid;
+  const int64_t r0 = g.rows.start, p = g.rows.len, c0 = g.cols.start, q = g.cols.len;
+  ZgemmDesc d;
+  d.N = ncols;
+  d.A = H; d.lda = ldh;
+  d.B = X; d.ldb = ldx;
+  d.C = Y; d.ldc = ldy;
+  d.alpha = alpha;
+  d.gamma = gamma;
+  d.S = X; d.lds = ldx;
+  if (dir == 0) {                       // W_i = alpha (H_ij V_j - gamma E_ij V_j) + beta W_i   (Eq. w=av)
+    d.M = (int)p; d.K = (int)q; d.conjA = false;
+    d.shift_lo = (int)std::max<int64_t>(0, c0 - r0);
+    d.shift_hi = (int)std::min<int64_t>(p, c0 + q - r0);
+    d.shift_off = r0 - c0;
+    d.beta = g.beta_owner_fwd() ? beta : 0.0;
+  } else {                              // V_j = alpha (H_ij^H W_i - gamma E_ij^T W_i) + beta V_j (Eq. v=aw)
+    d.M = (int)q; d.K = (int)p; d.conjA = true;
+    d.shift_lo = (int)std::max<int64_t>(0, r0 - c0);
+    d.shift_hi = (int)std::min<int64_t>(q, r0 + p - c0);
+    d.shift_off = c0 - r0;
+    d.beta = g.beta_owner_bwd() ? beta : 0.0;
+  }
+  if (gamma == 0.0 || d.shift_lo >= d.shift_hi) { d.S = nullptr; d.shift_lo = d.shift_hi = 0; }
+  zgemm(d, h->stream);
+  if (dir == 0)
+    allreduce_block(h, h->rowc, g.c, Y, p, ldy, ncols);     // row communicator
+  else
+    allreduce_block(h, h->colc, g.r, Y, q, ldy, ncols);     // column communicator
+}
+
+// ------------------------------------------------------------------------ Chebyshev filter
+// Scalars (ledger #1): c = (b_sup+mu_ne)/2, e = (b_sup-mu_ne)/2, sigma_1 =
+// e/(mu_1-c); k=1: alpha = sigma_1/e, beta = 0; k>=2: sigma_k = 1/(2/sigma_1 - sigma_{k-1}),
+// alpha = 2 sigma_k/e, beta = -sigma_{k-1} sigma_k; gamma = c.  Odd steps run forward
+// (V-layout -> W-layout), even steps backward (W -> V), so even degrees end in V.
+// Step k runs on the active suffix {a : m_a >= k} of the degree-sorted columns.
+int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, void* W,
+               int64_t ldw, int ncols, const int* degrees, double b_sup, double mu_1, double mu_ne) {
+  if (ncols <= 0) return 0;
+  int64_t matvecs = 0;
+  for (int a = 0; a < ncols; ++a) {
+    if (degrees[a] < 0 || (degrees[a] & 1)) throw UsageError("filter degrees must be even and >= 0");
+    if (a > 0 && degrees[a] < degrees[a - 1]) throw UsageError("filter degrees must be sorted ascending");
+    matvecs += degrees[a];
+  }
+  const int kmax = degrees[ncols - 1];
+  if (kmax == 0) return 0;
+  const double c = 0.5 * (b_sup + mu_ne), e = 0.5 * (b_sup - mu_ne);
+  if (!(e > 0.0)) throw UsageError("filter interval is empty (b_sup <= mu_ne)");
+  const double sigma1 = e / (mu_1 - c);
+  double sigma_prev = sigma1;
+  double2* Vz = reinterpret_cast<double2*>(V);
+  double2* Wz = reinterpret_cast<double2*>(W);
+  int first = 0;
+  for (int k = 1; k <= kmax; ++k) {
+    while (first < ncols && degrees[first] < k) ++first;
+    const int nk = ncols - first;
+    double alpha, beta;
+    if (k == 1) {
+      alpha = sigma1 / e;
+      beta = 0.0;
+    } else {
+      const double sigma = 1.0 / (2.0 / sigma1 - sigma_prev);
+      alpha = 2.0 * sigma / e;
+      beta = -sigma_prev * sigma;
+      sigma_prev = sigma;
+    }
+    if (k & 1)
+      hemm_step(h, 0, H, ldh, Vz + (int64_t)first * ldv, ldv, Wz + (int64_t)first * ldw, ldw, nk,
+                alpha, beta, c);
+    else
+      hemm_step(h, 1, H, ldh, Wz + (int64_t)first * ldw, ldw, Vz + (int64_t)first * ldv, ldv, nk,
+                alpha, beta, c);
+  }
+  return matvecs;
+}
+
+// -------------------------------------------------------------------- random start block
+__global__ void k_random_block(double2* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
+                               int ncols, uint32_t k0, uint32_t k1, uint32_t stream_id) {
+  const int64_t total = rows * ncols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rloc = idx % rows;
+    const int cl = (int)(idx / rows);
+    const uint64_t grow = (uint64_t)(grow0 + rloc);
+    const Philox4 o = philox4x32_10((uint32_t)grow, (uint32_t)(grow >> 32), (uint32_t)(col0 + cl),
+                                    stream_id, k0, k1);
+    V[rloc + (int64_t)cl * ldv] = make_double2(philox_unit(o.x[0], o.x[1]), philox_unit(o.x[2], o.x[3]));
+  }
+}
+
+void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
+                  int ncols, uint64_t seed, uint32_t stream_id) {
+  if (rows <= 0 || ncols <= 0) return;
+  const int64_t total = rows * ncols;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_random_block<<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double2*>(V), ldv, rows, grow0,
+                                                col0, ncols, (uint32_t)seed, (uint32_t)(seed >> 32),
+                                                stream_id);
+  CHASE_CHECK_LAUNCH();
+}
+
+}  // namespace chase
+
+// ============================================================================== C ABI
+namespace {
+
+// Collective status agreement: every rank returns the same status (chase.h "Validation").
+chase_status agree(chase_handle* h, chase_status st) {
+  if (!h || h->world_size <= 1 || !h->world || h->broken) return st;
+  try {
+    int* d = nullptr;
+    CHASE_CUDA(cudaMallocAsync(&d, sizeof(int), h->stream));
+    int v = (int)st;
+    CHASE_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+    CHASE_NCCL(ncclAllReduce(d, d, 1, ncclInt32, ncclMax, h->world, h->stream));
+    CHASE_CUDA(cudaMemcpyAsync(&v, d, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CHASE_CUDA(cudaFreeAsync(d, h->stream));
+    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    if (v != (int)st && h->err.empty()) h->err = "another rank failed with status " + std::to_string(v);
+    return (chase_status)v;
+  } catch (...) {
+    h->broken = true;
+    return CHASE_E_NCCL;
+  }
+}
+
+template <class F>
+chase_status guarded(chase_handle* h, F&& f, bool collective = true) {
+  if (!h) return CHASE_E_USAGE;
+  if (h->broken) { h->err = "handle is unusable after an earlier CUDA/NCCL error"; return CHASE_E_CUDA; }
+  chase_status st = CHASE_OK;
+  try {
+    CHASE_CUDA(cudaSetDevice(h->device));
+    st = f();
+  } catch (const UsageError& e) {
+    h->err = e.what(); st = CHASE_E_USAGE;
+  } catch (const NumericError& e) {
+    h->err = e.what(); st = CHASE_E_NUMERIC;
+  } catch (const NcclError& e) {
+    h->err = e.what(); st = CHASE_E_NCCL; h->broken = true;
+  } catch (const CudaError& e) {
+    h->err = e.what(); st = CHASE_E_CUDA; h->broken = true;
+  } catch (const std::bad_alloc&) {
+    h->err = "host out of memory"; st = CHASE_E_NOMEM;
+  } catch (const std::exception& e) {
+    h->err = e.what(); st = CHASE_E_CUDA; h->broken = true;
+  }
+  return collective ? agree(h, st) : st;
+}
+
+void order_after_user(chase_handle* h) {
+  if (h->user_stream && h->user_stream != h->stream) {
+    CHASE_CUDA(cudaEventRecord(h->ev0, h->user_stream));
+    CHASE_CUDA(cudaStreamWaitEvent(h->stream, h->ev0, 0));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* chase_version(void) { return "chase-b200 0.1 (sm_100a, FP64 DMMA + TMA)"; }
+
+const char* chase_last_error(const chase_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+chase_status chase_init(chase_handle** out, const chase_init_args* a) {
+  if (!out || !a) return CHASE_E_USAGE;
+  *out = nullptr;
+  chase_handle* h = new chase_handle();
+  try {
+    if (a->dtype != CHASE_C128) throw UsageError("only CHASE_C128 is implemented");
+    if (a->N <= 0 || a->nev_max <= 0 || a->nex_max <= 0 || a->nev_max + (int64_t)a->nex_max > a->N)
+      throw UsageError("invalid N / nev_max / nex_max");
+    int ws = std::max(1, a->world_size);
+    int r = a->grid_rows, c = a->grid_cols;
+    if (r <= 0 || c <= 0) { r = 1; c = ws; }
+    // world_size == 1 with r*c > 1: emulated-grid mode (one shard of an r x c grid, no
+    // communicators; collective sums are left to the caller).  Used by single-GPU grid tests.
+    if (r * c != ws && ws != 1) throw UsageError("grid_rows * grid_cols must equal world_size");
+    if (a->rank < 0 || a->rank >= r * c) throw UsageError("rank out of range");
+    if (a->N < std::max(r, c)) throw UsageError("N must be >= max(r, c)");
+    h->world_size = ws;
+    h->device = a->cuda_device;
+    CHASE_CUDA(cudaSetDevice(h->device));
+    int major = 0;
+    CHASE_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device));
+    if (major < 10) throw UsageError("this library requires an sm_100a (B200) device");
+    h->grid.setup(a->N, r, c, a->rank);
+    CHASE_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->user_stream = reinterpret_cast<cudaStream_t>(a->cuda_stream);
+    CHASE_CUDA(cudaEventCreate(&h->ev0));
+    CHASE_CUDA(cudaEventCreate(&h->ev1));
+    if (ws > 1) {
+      if (!a->nccl_unique_id) throw UsageError("nccl_unique_id required when world_size > 1");
+      ncclUniqueId id;
+      std::memcpy(&id, a->nccl_unique_id, sizeof(id));
+      CHASE_NCCL(ncclCommInitRank(&h->world, ws, id, a->rank));
+      CHASE_NCCL(ncclCommSplit(h->world, h->grid.i, h->grid.j, &h->rowc, nullptr));   // row comm i
+      CHASE_NCCL(ncclCommSplit(h->world, h->grid.j, h->grid.i, &h->colc, nullptr));   // column comm j
+    }
+    h->n_e_max = a->nev_max + a->nex_max;
+    // Workspace: V, V2 (V-layout q x n_e), W, HV (W-layout p x n_e), n_e x n_e
+    // matrices.  Memory check against free device memory (P:507-531 analogue).
+    const int64_t p = h->grid.rows.len, q = h->grid.cols.len, ne = h->n_e_max;
+    const size_t need = 16 * (size_t)(2 * q * ne + 2 * p * ne + 3 * ne * ne);
+    size_t fre = 0, tot = 0;
+    CHASE_CUDA(cudaMemGetInfo(&fre, &tot));
+    if (need > fre) throw std::bad_alloc();
+    h->V.alloc(16 * (size_t)q * ne);
+    h->V2.alloc(16 * (size_t)q * ne);
+    h->W.alloc(16 * (size_t)p * ne);
+    h->HV.alloc(16 * (size_t)p * ne);
+    h->G.alloc(16 * (size_t)ne * ne);
+    h->G2.alloc(16 * (size_t)ne * ne);
+    h->Z.alloc(16 * (size_t)ne * ne);
+  } catch (const UsageError& e) {
+    h->err = e.what();
+    *out = h;
+    return CHASE_E_USAGE;
+  } catch (const std::bad_alloc&) {
+    h->err = "workspace does not fit in device memory";
+    *out = h;
+    return CHASE_E_NOMEM;
+  } catch (const NcclError& e) {
+    h->err = e.what();
+    *out = h;
+    return CHASE_E_NCCL;
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    *out = h;
+    return CHASE_E_CUDA;
+  }
+  *out = h;
+  return CHASE_OK;
+}
+
+chase_status chase_set_option(chase_handle* h, const char* key, double v) {
+  return guarded(h, [&]() {
+    if (!key) throw UsageError("null option key");
+    std::string k(key);
+    if (k == "deg_max") { if (v < 2) throw UsageError("deg_max >= 2"); h->opt.deg_max = (int)v; }
+    else if (k == "max_iter") { if (v < 1) throw UsageError("max_iter >= 1"); h->opt.max_iter = (int)v; }
+    else if (k == "lanczos_steps") { if (v < 2) throw UsageError("lanczos_steps >= 2"); h->opt.lanczos_steps = (int)v; }
+    else if (k == "lanczos_runs") { if (v < 1) throw UsageError("lanczos_runs >= 1"); h->opt.lanczos_runs = (int)v; }
+    else if (k == "seed_v") h->opt.seed_v = (uint64_t)v;
+    else if (k == "seed_lanczos") h->opt.seed_lanczos = (uint64_t)v;
+    else if (k == "largest") h->opt.largest = v != 0.0;
+    else if (k == "approx") h->opt.approx = v != 0.0;
+    else throw UsageError("unknown option " + k);
+    return CHASE_OK;
+  }, false);
+}
+
+chase_status chase_local_layout(const chase_handle* h, int64_t* row0, int64_t* p, int64_t* col0,
+                                int64_t* q) {
+  if (!h) return CHASE_E_USAGE;
+  if (row0) *row0 = h->grid.rows.start;
+  if (p) *p = h->grid.rows.len;
+  if (col0) *col0 = h->grid.cols.start;
+  if (q) *q = h->grid.cols.len;
+  return CHASE_OK;
+}
+
+chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H, int64_t ldh,
+                             const void* X, int64_t ldx, void* Y, int64_t ldy, int32_t ncols,
+                             double alpha, double beta, double gamma) {
+  return guarded(h, [&]() {
+    const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
+    if (dir != 0 && dir != 1) throw UsageError("dir must be 0 or 1");
+    if (!H || !X || !Y || ncols < 0 || ldh < p) throw UsageError("bad pointers / sizes");
+    if (ldx < (dir == 0 ? q : p) || ldy < (dir == 0 ? p : q)) throw UsageError("bad leading dimension");
+    order_after_user(h);
+    hemm_step(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma);
+    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    return CHASE_OK;
+  });
+}
+
+chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv,
+                          void* W, int64_t ldw, int32_t ncols, const int32_t* degrees,
+                          double b_sup, double mu_1, double mu_ne, int64_t* matvecs) {
+  return guarded(h, [&]() {
+    const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
+    if (!H || !V || !W || ncols < 0 || (ncols > 0 && !degrees)) throw UsageError("bad pointers");
+    if (ldh < p || ldv < q || ldw < p) throw UsageError("bad leading dimension");
+    order_after_user(h);
+    const int64_t mv = filter(h, H, ldh, V, ldv, W, ldw, ncols, degrees, b_sup, mu_1, mu_ne);
+    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    if (matvecs) *matvecs = mv;
+    return CHASE_OK;
+  });
+}
+
+chase_status chase_lanczos(chase_handle* h, const void* H, int64_t ldh, int32_t n_e, double* b_sup,
+                           double* mu_1, double* mu_ne, double* nu) {
+  return guarded(h, [&]() {
+    if (!H || ldh < h->grid.rows.len || n_e <= 0 || n_e > h->grid.N) throw UsageError("bad arguments");
+    order_after_user(h);
+    LanczosOut o = lanczos(h, H, ldh, n_e);
+    if (b_sup) *b_sup = o.b_sup;
+    if (mu_1) *mu_1 = o.mu_1;
+    if (mu_ne) *mu_ne = o.mu_ne;
+    if (nu) *nu = o.nu;
+    return CHASE_OK;
+  });
+}
+
+chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t col0, int32_t ncols,
+                                uint64_t seed, uint32_t stream) {
+  return guarded(h, [&]() {
+    if (!V || ldv < h->grid.cols.len || ncols < 0) throw UsageError("bad arguments");
+    order_after_user(h);
+    random_block(h, V, ldv, h->grid.cols.len, h->grid.cols.start, col0, ncols, seed, stream);
+    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    return CHASE_OK;
+  }, false);
+}
+
+chase_status chase_solve(chase_handle* h, const void* H, int64_t ldh, int64_t N, int32_t nev,
+                         int32_t nex, int32_t deg, double tol, double* ritz_values,
+                         void* ritz_vectors, int64_t ldv, chase_report* report) {
+  return guarded(h, [&]() {
+    if (N != h->grid.N) throw UsageError("N differs from chase_init");
+    if (!(nev > 0 && nex > 0 && (int64_t)nev + nex <= N && tol > 0 && deg >= 1))
+      throw UsageError("invalid nev / nex / tol / deg (S:407)");
+    if (nev + nex > h->n_e_max) throw UsageError("nev + nex exceeds nev_max + nex_max of chase_init");
+    if (!H || ldh < h->grid.rows.len || !ritz_values || !ritz_vectors || ldv < h->grid.cols.len)
+      throw UsageError("bad pointers / leading dimensions");
+    order_after_user(h);
+    return solve(h, H, ldh, nev, nex, deg, tol, ritz_values, ritz_vectors, ldv, report);
+  });
+}
+
+chase_status chase_finalize(chase_handle* h) {
+  if (!h) return CHASE_E_USAGE;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz})
+    b->release();
+  if (h->rowc) ncclCommDestroy(h->rowc);
+  if (h->colc) ncclCommDestroy(h->colc);
+  if (h->world) ncclCommDestroy(h->world);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return CHASE_OK;
+}
+
+}  // extern "C"

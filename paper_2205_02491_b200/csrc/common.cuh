@@ -1,0 +1,36 @@
+// Common helpers for the ChASE B200 library (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "this library targets sm_100a (B200) only"
+#endif
+
+namespace chase {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CHASE_CUDA(call)                                                                      \
+  do {                                                                                        \
+    cudaError_t _e = (call);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      throw ::chase::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e) + " @" +    \
+                               __FILE__ + ":" + std::to_string(__LINE__));                    \
+  } while (0)
+
+#define CHASE_CHECK_LAUNCH() CHASE_CUDA(cudaGetLastError())
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// complex double stored interleaved (re, im) == double2 == torch.complex128
+using z_t = double2;
+
+__host__ __device__ inline double2 zmk(double r, double i) { return make_double2(r, i); }
+
+}  // namespace chase

@@ -1,0 +1,107 @@
+// Internal definition of chase_handle and the library's internal entry points.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdexcept>
+#include "common.cuh"
+#include <string>
+#include <vector>
+#include "../../include/chase.h"
+#include "grid.h"
+#include "zgemm.h"
+
+namespace chase {
+
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct UsageError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CHASE_NCCL(call)                                                                        \
+  do {                                                                                          \
+    ncclResult_t _r = (call);                                                                   \
+    if (_r != ncclSuccess)                                                                      \
+      throw ::chase::NcclError(std::string(#call) + ": " + ncclGetErrorString(_r));             \
+  } while (0)
+
+// Device buffer owned by the handle.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void alloc(size_t b) {
+    if (b <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CHASE_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct Options {
+  int deg_max = 36;
+  int max_iter = 100;
+  int lanczos_steps = 25;
+  int lanczos_runs = 4;
+  uint64_t seed_v = 2;
+  uint64_t seed_lanczos = 3;
+  bool largest = false;
+  bool approx = false;
+};
+
+}  // namespace chase
+
+struct chase_handle {
+  chase::Grid grid;
+  int device = 0;
+  int world_size = 1;
+  cudaStream_t stream = nullptr;       // library stream (all kernels, NCCL)
+  cudaStream_t user_stream = nullptr;  // caller stream to order against
+  ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
+  chase::Options opt;
+  int n_e_max = 0;
+  // workspace
+  chase::DBuf V, W, HV, V2, G, G2, Z, scratch, red, lz;
+  std::vector<double> host_scratch;
+  std::string err;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool broken = false;
+};
+
+namespace chase {
+
+// one fused distributed recurrence step (a2/a3 or a4/a5); see chase.h chase_hemm_step
+void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
+               void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma);
+// V <- Filter(...) (a1-a5)
+int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, void* W,
+               int64_t ldw, int ncols, const int* degrees, double b_sup, double mu_1, double mu_ne);
+// in-place sum over a communicator of a column block (rows x ncols, ld)
+void allreduce_block(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows,
+                     int64_t ld, int ncols);
+void allreduce_doubles(chase_handle* h, ncclComm_t comm, int comm_size, double* x, size_t n);
+
+struct LanczosOut {
+  double b_sup, mu_1, mu_ne, nu;
+};
+LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e);
+
+void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
+                  int ncols, uint64_t seed, uint32_t stream_id);
+
+chase_status solve(chase_handle* h, const void* H, int64_t ldh, int nev, int nex, int deg,
+                   double tol, double* ritz_values, void* ritz_vectors, int64_t ldv,
+                   chase_report* rep);
+
+}  // namespace chase

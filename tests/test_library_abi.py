@@ -1,0 +1,48 @@
+"""CPU checks of the boundary: the C-ABI library builds, loads and exports every symbol that
+include/chase.h declares (no compute calls: there is no GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "chase.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:chase_status|const char\*)\s+(chase_\w+)\s*\(", src, re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    names = _declared()
+    for n in ("chase_init", "chase_solve", "chase_finalize", "chase_set_option", "chase_local_layout",
+              "chase_last_error", "chase_filter", "chase_hemm_step", "chase_lanczos"):
+        assert n in names
+
+
+def test_library_loads_and_exports_all_declared_symbols():
+    import paper_2205_02491_b200 as pkg
+    lib = pkg.load()
+    for n in _declared():
+        assert hasattr(lib, n), n
+    assert set(pkg.EXPORTS) <= set(_declared())
+    assert "sm_100a" in pkg.version()
+
+
+def test_generator_twin_library_loads():
+    lib = ctypes.CDLL(os.path.join(ROOT, "chase_gen", "libchase_gen.so"))
+    assert hasattr(lib, "chase_gen_g2_block")
+
+
+def test_library_is_sm100a_only():
+    """The shipped cubin is sm_100a (cuobjdump lists the embedded ELF arch)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    so = os.path.join(ROOT, "paper_2205_02491_b200", "libchase_b200.so")
+    out = subprocess.run([exe, "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out

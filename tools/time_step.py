@@ -1,0 +1,29 @@
+"""Quick timing of one fused filter step (forward + backward) at a given shape on one B200."""
+import sys, time, json
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import paper_2205_02491_b200 as pkg
+from chase_gen import make_matrix
+from chase_gen.device import DeviceG2
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 30000
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 3000
+M = make_matrix("uniform", N, "g2", seed=1)
+dg = DeviceG2(M)
+H = torch.empty((N, N), dtype=torch.complex128, device="cuda").t()
+dg.fill(H, 0, 0)
+V = torch.randn((n, N), dtype=torch.complex128, device="cuda").t()
+W = torch.zeros((n, N), dtype=torch.complex128, device="cuda").t()
+ch = pkg.Chase(N, n - 10, 10)
+for d in (0, 1):
+    ch.hemm_step(d, H, V if d == 0 else W, W if d == 0 else V, n, 1e-3, 0.5, 0.3)
+torch.cuda.synchronize()
+for d in (0, 1):
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        ch.hemm_step(d, H, V if d == 0 else W, W if d == 0 else V, n, 1e-3, 0.5, 0.3)
+        ts.append(time.perf_counter() - t)
+    flops = 8.0 * N * N * n
+    print(json.dumps({"dir": d, "N": N, "n": n, "s": min(ts), "tflops": flops / min(ts) / 1e12}))
