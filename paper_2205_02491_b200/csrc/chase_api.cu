@@ -41,8 +41,10 @@ void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void*
   d.A = H; d.lda = ldh;
   d.B = X; d.ldb = ldx;
   d.C = Y; d.ldc = ldy;
-  d.alpha = alpha;
-  d.gamma = gamma;
+  // `largest` solves on -H (ledger #17): alpha((sH) X - gamma X) = (s alpha)(H X - (s gamma) X)
+  const double hs = h->opt.largest ? -1.0 : 1.0;
+  d.alpha = alpha * hs;
+  d.gamma = gamma * hs;
   d.S = X; d.lds = ldx;
   if (dir == 0) {                       // W_i = alpha (H_ij V_j - gamma E_ij V_j) + beta W_i   (Eq. w=av)
     d.M = (int)p; d.K = (int)q; d.conjA = false;

@@ -27,6 +27,8 @@ void hermitize(void* G, int64_t ld, int n, cudaStream_t st);
 // dst[:, a] = src[:, perm[a]] for a < ncols (perm on device)
 void permute_cols(void* dst, int64_t ldd, const void* src, int64_t lds, int64_t rows,
                   const int* perm, int ncols, cudaStream_t st);
+// G[i,i] += s for i < n
+void add_diag(void* G, int64_t ld, int n, double s, cudaStream_t st);
 // Lanczos helpers (full-length vectors, L runs side by side; see lanczos.cu)
 void scale_cols_inv(void* X, int64_t ld, int64_t rows, int ncols, const double* nrm2, cudaStream_t st);
 

@@ -1,0 +1,387 @@
+// Hermitian eigensolver for the Rayleigh-Ritz quotient G = Q^H A Q (Alg. 1 line 6)
+// on the device: block-cyclic two-sided Jacobi.
+//
+// The paper diagonalises G on the CPU with LAPACK divide & conquer.  Here it stays on
+// the GPU: the index set is split into 2b blocks of 32; each round pairs the blocks (circle
+// method) and, for every pair (P, Q), one CTA diagonalises the 64 x 64 subproblem
+// G[P u Q, P u Q] by cyclic Jacobi in shared memory (32 disjoint rotations per parallel step).
+// The resulting 64 x 64 unitaries U_k are then applied as G <- U^H G U with one 64 x 64 tile
+// product per (l <= k) block pair (Hermitian symmetry halves the work) and Z <- Z U.  Converged
+// when off(G)_F <= 1e-15 ||G||_F.  Deterministic (no atomics), so every rank that runs it
+// redundantly on identical inputs gets identical bits (ledger #20).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <vector>
+#include "common.cuh"
+#include "dense.h"
+#include "handle.h"
+#include "linalg.h"
+
+namespace chase {
+
+namespace {
+constexpr int W = 32;            // block width
+constexpr int S = 2 * W;         // subproblem size
+constexpr int LD = S + 1;        // padded smem row stride (complex)
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {   // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+__device__ __forceinline__ int64_t gidx(const int* pairs, int k, int t) {
+  // global index of local index t (0..63) of pair k: blocks P = pairs[2k], Q = pairs[2k+1]
+  return (int64_t)(t < W ? pairs[2 * k] * W + t : pairs[2 * k + 1] * W + (t - W));
+}
+
+// A = pad(G): A[0:n,0:n] = G, padded diagonal = distinct values above the spectrum; Z = I.
+__global__ void k_pad_init(const double2* G, int64_t ldg, int n, double2* A, double2* Z, int np, double padbase) {
+  const int64_t total = (int64_t)np * np;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % np), j = (int)(idx / np);
+    double2 v = make_double2(0.0, 0.0);
+    if (i < n && j < n) v = G[i + (int64_t)j * ldg];
+    else if (i == j) v = make_double2(padbase * (1.0 + (double)(i - n) / np), 0.0);
+    A[idx] = v;
+    Z[idx] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+}
+
+// One CTA per pair: diagonalise the 64 x 64 Hermitian subproblem by cyclic Jacobi; write U_k.
+__global__ void __launch_bounds__(256) k_sub_eig(const double2* A, int np, const int* pairs, double2* U) {
+  extern __shared__ double2 sm[];
+  double2* Sm = sm;              // S x LD
+  double2* Um = sm + S * LD;     // S x LD
+  __shared__ double rc[W], rs[W];
+  __shared__ double2 rph[W];
+  __shared__ double red[256];
+  const int k = blockIdx.x, t = threadIdx.x;
+  for (int idx = t; idx < S * S; idx += 256) {
+    const int i = idx % S, j = idx / S;
+    Sm[i * LD + j] = A[gidx(pairs, k, i) + gidx(pairs, k, j) * np];
+    Um[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  const int pr = t >> 3, sub = t & 7;     // 32 pairs x 8 threads
+  __shared__ int nrot;
+  if (t == 0) nrot = 0;
+  __syncthreads();
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    // convergence test: off-diagonal Frobenius norm vs total
+    double off = 0.0, tot = 0.0;
+    for (int idx = t; idx < S * S; idx += 256) {
+      const int i = idx % S, j = idx / S;
+      const double2 v = Sm[i * LD + j];
+      const double m2 = v.x * v.x + v.y * v.y;
+      tot += m2;
+      if (i != j) off += m2;
+    }
+    red[t] = off;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
+    const double offs = red[0];
+    __syncthreads();
+    red[t] = tot;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
+    const double tots = red[0];
+    __syncthreads();
+    if (offs <= 1e-32 * tots || offs == 0.0) break;
+    if (sweep > 0 && nrot == 0) break;          // previous sweep found nothing above threshold
+    __syncthreads();
+    if (t == 0) nrot = 0;
+    __syncthreads();
+    for (int r = 0; r < S - 1; ++r) {
+      // circle method: player S-1 fixed; pair 0 = (r, S-1); pair i = ((r+i) % 63, (r-i+63) % 63)
+      int p, q;
+      if (pr == 0) { p = r; q = S - 1; }
+      else { p = (r + pr) % (S - 1); q = (r - pr + (S - 1)) % (S - 1); }
+      if (p > q) { const int tmp = p; p = q; q = tmp; }
+      if (sub == 0) {
+        const double a = Sm[p * LD + p].x, d = Sm[q * LD + q].x;
+        const double2 b = Sm[p * LD + q];
+        const double ab = hypot(b.x, b.y);
+        double c = 1.0, s = 0.0;
+        double2 ph = make_double2(1.0, 0.0);     // e^{-i phi}
+        // rotate only if |a_pq| is significant relative to the diagonal (Demmel-Veselic)
+        if (ab > 1e-300 && ab > 2e-16 * sqrt(fabs(a) * fabs(d))) {
+          atomicAdd(&nrot, 1);
+          const double tau = (d - a) / (2.0 * ab);
+          const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
+          c = 1.0 / hypot(1.0, tt);
+          s = tt * c;
+          ph = make_double2(b.x / ab, -b.y / ab);
+        }
+        rc[pr] = c; rs[pr] = s; rph[pr] = ph;
+      }
+      __syncthreads();
+      const double c = rc[pr], s = rs[pr];
+      const double2 ph = rph[pr];
+      // columns:  x_p' = c x_p - s e^{-i phi} x_q ;  x_q' = s x_p + c e^{-i phi} x_q   (S and U)
+      for (int i = sub; i < S; i += 8) {
+        {
+          const double2 xp = Sm[i * LD + p], xq = cmul(ph, Sm[i * LD + q]);
+          Sm[i * LD + p] = make_double2(c * xp.x - s * xq.x, c * xp.y - s * xq.y);
+          Sm[i * LD + q] = make_double2(s * xp.x + c * xq.x, s * xp.y + c * xq.y);
+        }
+        {
+          const double2 xp = Um[i * LD + p], xq = cmul(ph, Um[i * LD + q]);
+          Um[i * LD + p] = make_double2(c * xp.x - s * xq.x, c * xp.y - s * xq.y);
+          Um[i * LD + q] = make_double2(s * xp.x + c * xq.x, s * xp.y + c * xq.y);
+        }
+      }
+      __syncthreads();
+      // rows:  y_p' = c y_p - s e^{+i phi} y_q ;  y_q' = s y_p + c e^{+i phi} y_q
+      const double2 phc = make_double2(ph.x, -ph.y);
+      for (int j = sub; j < S; j += 8) {
+        const double2 yp = Sm[p * LD + j], yq = cmul(phc, Sm[q * LD + j]);
+        Sm[p * LD + j] = make_double2(c * yp.x - s * yq.x, c * yp.y - s * yq.y);
+        Sm[q * LD + j] = make_double2(s * yp.x + c * yq.x, s * yp.y + c * yq.y);
+      }
+      __syncthreads();
+    }
+  }
+  double2* Uk = U + (int64_t)k * S * S;
+  for (int idx = t; idx < S * S; idx += 256) {
+    const int i = idx % S, j = idx / S;
+    Uk[idx] = Um[i * LD + j];          // column-major 64 x 64
+  }
+}
+
+// 64x64x64 complex tile product in shared memory: out = op(X) * Y, op = identity or ^H.
+// 256 threads; thread (tx, ty) owns rows ty + 16 r, cols tx + 16 c (r, c < 4).
+template <bool CONJX>
+__device__ __forceinline__ void tile_mm(const double2* X, const double2* Y, double2 (&acc)[4][4]) {
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = make_double2(0.0, 0.0);
+#pragma unroll 4
+  for (int m = 0; m < S; ++m) {
+    double2 xv[4], yv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) xv[r] = CONJX ? X[m * LD + ty + 16 * r] : X[(ty + 16 * r) * LD + m];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) yv[c] = Y[m * LD + tx + 16 * c];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double2 u = CONJX ? cmulc(xv[r], yv[c]) : cmul(xv[r], yv[c]);
+        acc[r][c].x += u.x;
+        acc[r][c].y += u.y;
+      }
+  }
+}
+
+// A[I_l, I_k] <- U_l^H A[I_l, I_k] U_k for l <= k (and the mirror block for l < k).
+__global__ void __launch_bounds__(256) k_apply_sym(double2* A, int np, const int* pairs, const double2* U, int b) {
+  extern __shared__ double2 sm[];
+  double2* Xs = sm;              // S x LD : A block, then T1
+  double2* Ys = sm + S * LD;     // S x LD : U_k, then U_l
+  // map blockIdx.x -> (l, k), l <= k
+  int idx = blockIdx.x, l = 0;
+  while (idx >= b - l) { idx -= b - l; ++l; }
+  const int k = l + idx;
+  const int t = threadIdx.x;
+  const double2* Uk = U + (int64_t)k * S * S;
+  const double2* Ul = U + (int64_t)l * S * S;
+  for (int e = t; e < S * S; e += 256) {
+    const int i = e % S, j = e / S;
+    Xs[i * LD + j] = A[gidx(pairs, l, i) + gidx(pairs, k, j) * np];
+    Ys[i * LD + j] = Uk[i + j * S];
+  }
+  __syncthreads();
+  double2 acc[4][4];
+  tile_mm<false>(Xs, Ys, acc);                 // T1 = A_lk U_k
+  __syncthreads();
+  const int tx = t & 15, ty = t >> 4;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) Xs[(ty + 16 * r) * LD + tx + 16 * c] = acc[r][c];
+  for (int e = t; e < S * S; e += 256) {
+    const int i = e % S, j = e / S;
+    Ys[i * LD + j] = Ul[i + j * S];
+  }
+  __syncthreads();
+  tile_mm<true>(Ys, Xs, acc);                  // T = U_l^H T1
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = ty + 16 * r, j = tx + 16 * c;
+      const int64_t gi = gidx(pairs, l, i), gj = gidx(pairs, k, j);
+      A[gi + gj * np] = acc[r][c];
+      if (l != k) A[gj + gi * np] = make_double2(acc[r][c].x, -acc[r][c].y);
+    }
+}
+
+// Z[rows rt*64 .. +64, I_k] <- Z[rows, I_k] U_k
+__global__ void __launch_bounds__(256) k_apply_z(double2* Z, int np, const int* pairs, const double2* U) {
+  extern __shared__ double2 sm[];
+  double2* Xs = sm;
+  double2* Ys = sm + S * LD;
+  const int rt = blockIdx.x, k = blockIdx.y, t = threadIdx.x;
+  const double2* Uk = U + (int64_t)k * S * S;
+  for (int e = t; e < S * S; e += 256) {
+    const int i = e % S, j = e / S;
+    Xs[i * LD + j] = Z[(int64_t)(rt * S + i) + gidx(pairs, k, j) * np];
+    Ys[i * LD + j] = Uk[i + j * S];
+  }
+  __syncthreads();
+  double2 acc[4][4];
+  tile_mm<false>(Xs, Ys, acc);
+  const int tx = t & 15, ty = t >> 4;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      Z[(int64_t)(rt * S + ty + 16 * r) + gidx(pairs, k, tx + 16 * c) * np] = acc[r][c];
+}
+
+// partial sums of |A_ij|^2: off-diagonal and total, per block of rows (fixed order)
+__global__ void k_offnorm(const double2* A, int np, double* part) {
+  __shared__ double s_off[256], s_tot[256];
+  const int col = blockIdx.x;
+  double off = 0.0, tot = 0.0;
+  for (int i = threadIdx.x; i < np; i += 256) {
+    const double2 v = A[i + (int64_t)col * np];
+    const double m2 = v.x * v.x + v.y * v.y;
+    tot += m2;
+    if (i != col) off += m2;
+  }
+  s_off[threadIdx.x] = off;
+  s_tot[threadIdx.x] = tot;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) { s_off[threadIdx.x] += s_off[threadIdx.x + s]; s_tot[threadIdx.x] += s_tot[threadIdx.x + s]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { part[2 * col] = s_off[0]; part[2 * col + 1] = s_tot[0]; }
+}
+
+__global__ void k_extract(const double2* A, const double2* Zp, int np, int n, const int* order, double* theta,
+                          double2* Z, int64_t ldz) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    const int src = order[j];
+    Z[i + (int64_t)j * ldz] = Zp[i + (int64_t)src * np];
+    if (i == 0) theta[j] = A[src + (int64_t)src * np].x;
+  }
+}
+
+struct Work {
+  void* A = nullptr; void* Zp = nullptr; void* U = nullptr; int* pairs = nullptr; int* order = nullptr;
+  double* part = nullptr;
+  size_t np = 0, b = 0;
+  void ensure(int np_, cudaStream_t) {
+    if ((size_t)np_ <= np) return;
+    release();
+    np = np_;
+    b = np / S;
+    CHASE_CUDA(cudaMalloc(&A, 16 * np * np));
+    CHASE_CUDA(cudaMalloc(&Zp, 16 * np * np));
+    CHASE_CUDA(cudaMalloc(&U, 16 * (size_t)S * S * b));
+    CHASE_CUDA(cudaMalloc(&pairs, sizeof(int) * 2 * b * (2 * b)));
+    CHASE_CUDA(cudaMalloc(&order, sizeof(int) * np));
+    CHASE_CUDA(cudaMalloc(&part, sizeof(double) * 2 * np));
+  }
+  void release() {
+    for (void* p : {A, Zp, U, (void*)pairs, (void*)order, (void*)part}) if (p) cudaFree(p);
+    A = Zp = U = nullptr; pairs = order = nullptr; part = nullptr; np = b = 0;
+  }
+};
+Work g_work;   // one solve at a time per process (the library is single-threaded per handle)
+}  // namespace
+
+int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int np = ceil_div(n, S) * S;
+  const int b = np / S;           // pairs per round; 2b blocks of W
+  const int nblocks = 2 * b;
+  g_work.ensure(np, st);
+  static bool attr = false;
+  const int smem = (int)(2 * sizeof(double2) * S * LD);
+  if (!attr) {
+    CHASE_CUDA(cudaFuncSetAttribute(k_sub_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CHASE_CUDA(cudaFuncSetAttribute(k_apply_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CHASE_CUDA(cudaFuncSetAttribute(k_apply_z, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  // schedule: circle method over 2b blocks, 2b-1 rounds of b pairs
+  const int rounds = nblocks - 1;
+  std::vector<int> sched(2 * (size_t)b * rounds);
+  for (int r = 0; r < rounds; ++r) {
+    for (int i = 0; i < b; ++i) {
+      int p, q;
+      if (i == 0) { p = r; q = nblocks - 1; }
+      else { p = (r + i) % (nblocks - 1); q = (r - i + (nblocks - 1)) % (nblocks - 1); }
+      sched[2 * ((size_t)r * b + i)] = std::min(p, q);
+      sched[2 * ((size_t)r * b + i) + 1] = std::max(p, q);
+    }
+  }
+  CHASE_CUDA(cudaMemcpyAsync(g_work.pairs, sched.data(), sizeof(int) * sched.size(), cudaMemcpyHostToDevice, st));
+  // padding above the spectrum: diagonal entries > ||G||_F >= ||G||_2, decoupled from G
+  double2* A = reinterpret_cast<double2*>(g_work.A);
+  double2* Zp = reinterpret_cast<double2*>(g_work.Zp);
+  k_pad_init<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const double2*>(G), ld, n, A, Zp, np, 0.0);
+  CHASE_CHECK_LAUNCH();
+  k_offnorm<<<np, 256, 0, st>>>(A, np, g_work.part);
+  CHASE_CHECK_LAUNCH();
+  std::vector<double> part(2 * (size_t)np);
+  CHASE_CUDA(cudaMemcpyAsync(part.data(), g_work.part, sizeof(double) * 2 * np, cudaMemcpyDeviceToHost, st));
+  CHASE_CUDA(cudaStreamSynchronize(st));
+  double tot = 0.0;
+  for (int j = 0; j < np; ++j) tot += part[2 * j + 1];
+  const double fro = std::sqrt(tot);
+  if (!std::isfinite(fro)) throw NumericError("Rayleigh-Ritz matrix is not finite");
+  const double padbase = (fro > 0.0 ? fro : 1.0) * 1.1;   // > ||G||_F >= ||G||_2 >= every |eigenvalue|
+  k_pad_init<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const double2*>(G), ld, n, A, Zp, np, padbase);
+  CHASE_CHECK_LAUNCH();
+
+  int sweeps = 0;
+  bool converged = false;
+  for (; sweeps < 40; ++sweeps) {
+    k_offnorm<<<np, 256, 0, st>>>(A, np, g_work.part);
+    CHASE_CHECK_LAUNCH();
+    CHASE_CUDA(cudaMemcpyAsync(part.data(), g_work.part, sizeof(double) * 2 * np, cudaMemcpyDeviceToHost, st));
+    CHASE_CUDA(cudaStreamSynchronize(st));
+    double off = 0.0, t2 = 0.0;
+    for (int j = 0; j < np; ++j) { off += part[2 * j]; t2 += part[2 * j + 1]; }
+    // off(A)_F <= 1e-14 ||A||_F (A = padded G; unitarily invariant)
+    if (off <= 1e-28 * t2) { converged = true; break; }
+    if (sweeps >= 12 && off <= 1e-24 * t2) { converged = true; break; }   // rounding floor reached
+    for (int r = 0; r < rounds; ++r) {
+      const int* pr = g_work.pairs + 2 * (size_t)r * b;
+      double2* U = reinterpret_cast<double2*>(g_work.U);
+      k_sub_eig<<<b, 256, smem, st>>>(A, np, pr, U);
+      CHASE_CHECK_LAUNCH();
+      k_apply_sym<<<b * (b + 1) / 2, 256, smem, st>>>(A, np, pr, U, b);
+      CHASE_CHECK_LAUNCH();
+      k_apply_z<<<dim3(np / S, b), 256, smem, st>>>(Zp, np, pr, U);
+      CHASE_CHECK_LAUNCH();
+    }
+  }
+  if (!converged) throw NumericError("block Jacobi did not converge in 40 sweeps");
+  // eigenvalues: diag(A); sort ascending, drop the padding (largest)
+  std::vector<double2> diag(np);
+  CHASE_CUDA(cudaMemcpy2DAsync(diag.data(), sizeof(double2), A, sizeof(double2) * (np + 1), sizeof(double2), np,
+                               cudaMemcpyDeviceToHost, st));
+  CHASE_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> order(np);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return diag[a].x < diag[c].x; });
+  CHASE_CUDA(cudaMemcpyAsync(g_work.order, order.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  k_extract<<<148 * 8, 256, 0, st>>>(A, Zp, np, n, g_work.order, theta, reinterpret_cast<double2*>(Z), ldz);
+  CHASE_CHECK_LAUNCH();
+  CHASE_CUDA(cudaStreamSynchronize(st));   // `order` / `diag` host buffers go out of scope
+  return sweeps;
+}
+
+}  // namespace chase
