@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native ChASE hot path.
+
+Step = one ChASE subspace iteration on resident H (the paper's one-iteration protocol,
+P:727-731): Lanczos bounds + filter (deg 20 on all nev+nex columns) + CholQR2 + Rayleigh-Ritz +
+residuals + locking -- every SURVEY §8(a) row -- through the C ABI (chase_solve, max_iter = 1).
+
+Workload (BASELINE.json configs[1]): complex double, Uniform spectrum (Table 1, d_max=1,
+eps=1e-4), N = 30000, nev = 2250, nex = 750, deg = 20, on one B200.  For N>1 GPUs the paper's weak
+scaling is used: N = 30000*sqrt(G) on an r x c grid (1x2, 2x2, 2x4), so the H shard per
+GPU stays 14.4 GB and per-GPU filter work is fixed.
+
+metric/value: filter TFLOP/s of the whole job = 8 N^2 matvecs / step time (max over ranks), with
+the step time measured on the device (CUDA events inside the library, on its stream).
+
+Launch:  python bench.py [--gpus N --steps K --warmup W]          (N = 1)
+         torchrun --nproc-per-node N ... bench.py --gpus N ...     (N > 1)
+         python bench.py --impl reference ...                      (the CPU oracle arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N1, NEV, NEX, DEG = 30000, 2250, 750, 20
+FP64_DMMA_PEAK_TFLOPS = 37.12     # measured (profiles/r01_fp64_peak.jsonl), see DESIGN.md
+METRIC = "filter TFLOP/s, one ChASE subspace iteration (P:727-731), complex double"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="chase", choices=["chase", "reference"])
+    ap.add_argument("--n", type=int, default=N1, help="matrix order on 1 GPU (weak-scaled for more)")
+    ap.add_argument("--nev", type=int, default=NEV)
+    ap.add_argument("--nex", type=int, default=NEX)
+    ap.add_argument("--family", default="uniform")
+    ap.add_argument("--tts", action="store_true", help="also run a full solve to convergence (time-to-solution)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = set(gpus)
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                idx = int(f[0])
+            except ValueError:
+                continue
+            if self.gpus and idx not in self.gpus:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        under_load = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": statistics.median(under_load) if under_load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle sample
+def oracle_sample(N, seconds=12.0, rows=1024, ncols=64, family="uniform"):
+    """The oracle's filter step (oracle.hemm_step, numpy complex128 on the host cores) on a
+    bounded sample of the workload: a `rows` x N row panel of H (generated untimed from the same
+    seeded G2 description) times a 64-column block, repeated for ~`seconds`.  Returns TFLOP/s."""
+    import numpy as np
+    import oracle
+    from chase_gen.dense import G2Matrix
+    from chase_gen.spectra import spectrum
+    M = G2Matrix(spectrum(family, N), seed=1)
+    Hp = M.block(0, rows, 0, N)
+    X = oracle.random_block(2, 0, N, 0, ncols, 0)
+    Y = np.zeros((rows, ncols), dtype=np.complex128)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        Y = oracle.hemm_step_rows(Hp, 0, X, Y, 0.5, -0.2, 0.3)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    flops = 8.0 * rows * N * ncols * n
+    cores = len(os.sched_getaffinity(0))
+    return flops / el / 1e12, cores, f"{n} oracle filter steps (hemm_step, P:385-390) on a {rows} x {N} row panel of H times {ncols} columns, numpy complex128"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    world = args.gpus
+    from paper_2205_02491_b200.dist import weak_scaled_n, grid_shape
+    N = weak_scaled_n(args.n, world)
+    per = max(3.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(N, seconds=per / 3, family=args.family)
+    vals, cores, sample = [], 0, ""
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, cores, sample = oracle_sample(N, seconds=per, family=args.family)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    v = statistics.mean(vals)
+    r, c = grid_shape(world)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded G2 generator, Table 1 spectrum)",
+            "config": {"workload": f"config2 (weak-scaled): N={N} complex double {args.family}, nev={args.nev}, nex={args.nex}, deg={DEG}; oracle filter-step sample",
+                       "N": N, "grid": f"{r}x{c}"},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2205_02491_b200 as pkg
+    from paper_2205_02491_b200.dist import grid_shape, weak_scaled_n, shard, broadcast_nccl_id, max_over_ranks
+    from chase_gen.dense import G2Matrix
+    from chase_gen.spectra import spectrum
+    from chase_gen.device import DeviceG2
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    grid = grid_shape(world)
+    N = weak_scaled_n(args.n, world)
+    nev, nex = args.nev, args.nex
+    row0, p, col0, q = shard(N, grid, rank)
+
+    # ---- input: H shard generated on the device from the seeded G2 description (untimed)
+    M = G2Matrix(spectrum(args.family, N), seed=1)
+    H = torch.empty((q, p), dtype=torch.complex128, device="cuda").t()        # p x q column-major
+    DeviceG2(M).fill(H, row0, col0)
+    torch.cuda.synchronize()
+    nccl_id = broadcast_nccl_id(rank) if world > 1 else None
+    stream = torch.cuda.current_stream().cuda_stream
+    ch = pkg.Chase(N, nev, nex, grid=grid, rank=rank, world_size=world, nccl_id=nccl_id, device=local,
+                   stream=stream)
+    assert ch.local_layout() == (row0, p, col0, q)
+    ch.set_option("max_iter", 1)
+    vecs = torch.empty((nev + nex, q), dtype=torch.complex128, device="cuda").t()
+
+    def step():
+        vals, _, rep, st = ch.solve(H, nev, nex, deg=DEG, tol=1e-10, vectors=vecs)
+        return rep
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    # ---- timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    ids = [int(x) for x in vis.split(",") if x.strip().isdigit()] if vis else list(range(world))
+    sampler = ClockSampler(ids[:world] if ids else [])
+    sampler.start()
+    time.sleep(0.3)
+    l0 = pkg.kernel_launches()
+    t_wall0 = time.perf_counter()
+    reps = [step() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall = time.perf_counter() - t_wall0
+    launches = pkg.kernel_launches() - l0
+    clocks = sampler.stop()
+    dev_s = sum(r["t_all"] for r in reps)
+    filt_s = sum(r["t_filter"] for r in reps)
+    matvecs = sum(r["matvecs"] for r in reps)
+    flops = 8.0 * N * N * matvecs
+    dev_s_max = max_over_ranks(dev_s)
+    filt_s_max = max_over_ranks(filt_s)
+    value = flops / dev_s_max / 1e12
+    phases = {k: max_over_ranks(sum(r[k] for r in reps)) / args.steps
+              for k in ("t_lanczos", "t_filter", "t_qr", "t_rr", "t_resid", "t_all")}
+
+    # ---- end-to-end through the C ABI with host buffers (H2D of H + D2H of the eigenpairs)
+    e2e = None
+    if not args.no_e2e:
+        Hh = torch.empty((q, p), dtype=torch.complex128, pin_memory=True).t()
+        Hh.copy_(H)
+        Hd = torch.empty_like(H)
+        vh = torch.empty((nev, q), dtype=torch.complex128, pin_memory=True).t()
+        e2e_steps = max(1, min(args.steps, 2))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        mv = 0
+        for _ in range(e2e_steps):
+            Hd.copy_(Hh, non_blocking=True)
+            vals, _, rep, st = ch.solve(Hd, nev, nex, deg=DEG, tol=1e-10, vectors=vecs)
+            vh.copy_(vecs[:, :nev], non_blocking=True)
+            mv += rep["matvecs"]
+        ev1.record()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(max(ev0.elapsed_time(ev1) * 1e-3, time.perf_counter() - t0))
+        e2e = {"value": 8.0 * N * N * mv / e2e_s / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 16 * p * q, "d2h_bytes_per_step": 16 * q * nev + 8 * nev,
+               "steps": e2e_steps}
+        del Hh, Hd, vh
+
+    # ---- roofline of the dominant kernel (filter GEMM): algorithmic FLOPs / measured filter time
+    per_launch_flops = 8.0 * p * q * (nev + nex)        # first iteration: every column at every degree step
+    launches_filter = DEG * args.steps
+    achieved = flops / world / filt_s_max / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_filter_gemm.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    tts = None
+    if args.tts:
+        ch.set_option("max_iter", 100)
+        t0 = time.perf_counter()
+        vals, _, rep, st = ch.solve(H, nev, nex, deg=DEG, tol=1e-10, vectors=vecs)
+        lam = M.lam[:nev]
+        tts = {"s": max_over_ranks(rep["t_all"]), "status": st, "iterations": rep["iterations"],
+               "matvecs": rep["matvecs"], "filter_tflops_per_gpu": 8.0 * N * N * rep["matvecs"] / world / max(rep["t_filter"], 1e-12) / 1e12,
+               "max_abs_eig_err_rel": float(np.max(np.abs(vals - lam)) / np.max(np.abs(M.lam)))}
+    ch.close()
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": dev_s_max / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+                "data": "synthetic (seeded G2 generator: H = Phi P C P^H Phi^H with the Table 1 Uniform spectrum, d_max=1, eps=1e-4)",
+                "config": {"workload": f"config2{' (weak-scaled)' if world > 1 else ''}: N={N} complex double {args.family}, nev={nev}, nex={nex}, deg={DEG}, one subspace iteration (P:727-731)",
+                           "N": N, "nev": nev, "nex": nex, "deg": DEG, "grid": f"{grid[0]}x{grid[1]}",
+                           "l2": "inputs larger than L2 (H shard %.1f GB >> 126 MB)" % (16e-9 * p * q)},
+                "wall_ms_per_step": t_wall / args.steps * 1e3,
+                "phases_s_per_step": phases,
+                "filter_tflops_per_gpu": achieved,
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                             "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": traffic,
+                             "kernel": "zgemm_dmma_kernel (filter step, FP64 DMMA.8x8x4 + TMA)",
+                             "per_launch_flops": per_launch_flops, "launches": launches_filter,
+                             "peak_source": "measured FP64 DMMA.8x8x4 loop on all 148 SMs (profiles/r01_fp64_peak.jsonl); MEASURED_PEAKS.json has no FP64 entry"},
+                "clocks": clocks, "gpu_launches": launches, "e2e": e2e}
+        if tts:
+            line["time_to_solution"] = tts
+        if world == 1 and not args.no_cpu:
+            v, cores, sample = oracle_sample(N, seconds=12.0, family=args.family)
+            line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -133,6 +133,14 @@ const char* chase_last_error(const chase_handle* h);
 /* Library build/version string (for diagnostics). */
 const char* chase_version(void);
 
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (call on rank 0, broadcast to all ranks
+ * out of band, pass as chase_init_args.nccl_unique_id).  Local. */
+chase_status chase_nccl_unique_id(void* out128);
+
+/* Number of CUDA kernels this process has launched through the library so far (diagnostic;
+ * used by the benchmark to report how many of its own kernels ran in the timed region). */
+unsigned long long chase_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

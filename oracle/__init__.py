@@ -19,7 +19,7 @@ and matvecs (Table 2, P:658-661 / P:685-688) -- they depend on unpublished DEMAG
 on heuristics the paper does not state (ledger #10); DESIGN.md lists them.
 """
 from .chase import (  # noqa: F401
-    filter_interval, filter_coefficients, hemm_step, chebyshev_filter, chebyshev_T,
+    filter_interval, filter_coefficients, hemm_step, hemm_step_rows, chebyshev_filter, chebyshev_T,
     lanczos, LanczosResult, qr_locked, rayleigh_ritz, residual_norms, optimal_degrees,
     lock_prefix, chase_solve, Report,
 )

@@ -60,6 +60,16 @@ def hemm_step(H, X, Yprev, alpha, beta, gamma):
     return Y
 
 
+def hemm_step_rows(H_rows, row0, X, Yprev_rows, alpha, beta, gamma):
+    """Rows [row0, row0 + H_rows.shape[0]) of hemm_step (the same definition restricted to a
+    row panel of H; used for bounded CPU timing samples at sizes where H does not fit)."""
+    nr = H_rows.shape[0]
+    Y = alpha * (H_rows @ X - gamma * X[row0:row0 + nr])
+    if beta != 0.0:
+        Y = Y + beta * Yprev_rows
+    return Y
+
+
 def chebyshev_filter(H, V, degrees, b_sup, mu_1, mu_ne):
     """V-hat <- Filter(A, b_sup, mu_1, mu_ne, V-hat, m)  (Alg. 1 line 4).
     Column a receives the degree-m_a polynomial; a column leaves the product as soon as its

@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "CHASE_OK", 2: "CHASE_E_USAGE", 3: "CHASE_E_NUMERIC", 4: "CHA
 # exported symbols (include/chase.h); tests check that every one is present
 EXPORTS = ("chase_init", "chase_set_option", "chase_local_layout", "chase_solve", "chase_hemm_step",
            "chase_filter", "chase_lanczos", "chase_random_block", "chase_finalize",
-           "chase_last_error", "chase_version")
+           "chase_last_error", "chase_version", "chase_nccl_unique_id", "chase_kernel_launches")
 
 
 class ChaseError(RuntimeError):
@@ -71,8 +71,11 @@ def load():
     lib.chase_last_error.argtypes = [vp]
     lib.chase_last_error.restype = C.c_char_p
     lib.chase_version.restype = C.c_char_p
+    lib.chase_nccl_unique_id.argtypes = [vp]
+    lib.chase_kernel_launches.argtypes = []
+    lib.chase_kernel_launches.restype = C.c_ulonglong
     for name in EXPORTS:
-        if name not in ("chase_last_error", "chase_version"):
+        if name not in ("chase_last_error", "chase_version", "chase_kernel_launches"):
             getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -190,3 +193,16 @@ class Chase:
 
 def version():
     return load().chase_version().decode()
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId from the library's NCCL (rank 0 only; broadcast it)."""
+    buf = C.create_string_buffer(128)
+    st = load().chase_nccl_unique_id(buf)
+    if st != CHASE_OK:
+        raise ChaseError(st, "ncclGetUniqueId failed")
+    return bytes(buf.raw)
+
+
+def kernel_launches():
+    return int(load().chase_kernel_launches())

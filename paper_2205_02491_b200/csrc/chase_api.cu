@@ -9,6 +9,8 @@ using namespace chase;
 
 namespace chase {
 
+unsigned long long g_kernel_launches = 0;
+
 // ------------------------------------------------------------------------------ collectives
 void allreduce_block(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows,
                      int64_t ld, int ncols) {
@@ -199,6 +201,16 @@ void order_after_user(chase_handle* h) {
 }  // namespace
 
 extern "C" {
+
+unsigned long long chase_kernel_launches(void) { return chase::g_kernel_launches; }
+
+chase_status chase_nccl_unique_id(void* out128) {
+  if (!out128) return CHASE_E_USAGE;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return CHASE_E_NCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return CHASE_OK;
+}
 
 const char* chase_version(void) { return "chase-b200 0.1 (sm_100a, FP64 DMMA + TMA)"; }
 

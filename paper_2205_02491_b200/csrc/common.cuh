@@ -24,7 +24,14 @@ struct CudaError : std::runtime_error {
                                __FILE__ + ":" + std::to_string(__LINE__));                    \
   } while (0)
 
-#define CHASE_CHECK_LAUNCH() CHASE_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by CHASE_CHECK_LAUNCH(), which also counts it
+// (exported as chase_kernel_launches() for the benchmark's gpu_launches claim).
+extern unsigned long long g_kernel_launches;
+#define CHASE_CHECK_LAUNCH()            \
+  do {                                  \
+    ++::chase::g_kernel_launches;       \
+    CHASE_CUDA(cudaGetLastError());     \
+  } while (0)
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 

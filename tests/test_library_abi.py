@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "chase.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:chase_status|const char\*)\s+(chase_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:chase_status|const char\*|unsigned long long)\s+(chase_\w+)\s*\(", src, re.M)))
 
 
 def test_header_declares_expected_entry_points():
