@@ -1,0 +1,102 @@
+"""Multi-GPU parity check of the distributed path (one process per GPU, NCCL inside the library).
+
+Run:  torchrun --nproc-per-node G --master-addr 127.0.0.1 --master-port 29511 tools/mgpu_check.py
+Each rank owns H_ij of an r x c grid; rank 0 compares the distributed fused steps, filter and
+chase_solve with the CPU oracle / exact spectrum.  Prints one JSON line per check on rank 0 and
+exits non-zero on any failure."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import paper_2205_02491_b200 as pkg  # noqa: E402
+from paper_2205_02491_b200.dist import grid_shape, shard, broadcast_nccl_id  # noqa: E402
+from chase_gen import make_matrix  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.asfortranarray(a)).t().contiguous().t().cuda()
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    grid = grid_shape(world)
+    N, nev, nex = int(os.environ.get("MG_N", "1201")), 40, 20
+    M = make_matrix("wilkinson", N, "g2", seed=3)
+    H = M.dense()
+    r0, p, c0, q = shard(N, grid, rank)
+    nid = broadcast_nccl_id(rank)
+    ch = pkg.Chase(N, nev, nex, grid=grid, rank=rank, world_size=world, nccl_id=nid, device=local)
+    assert ch.local_layout() == (r0, p, c0, q)
+    dH = dev(H[r0:r0 + p, c0:c0 + q])
+    ok = True
+    out = []
+    rng = np.random.default_rng(0)
+    n = 37
+    X = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
+    Y0 = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
+    ref = oracle.hemm_step(H, X, Y0, 0.7, -0.3, 0.45)
+    # forward: X V-layout (rows c0..), Y W-layout (rows r0..)
+    dY = dev(Y0[r0:r0 + p])
+    ch.hemm_step(0, dH, dev(X[c0:c0 + q]), dY, n, 0.7, -0.3, 0.45)
+    e_f = np.linalg.norm(dY.cpu().numpy() - ref[r0:r0 + p]) / np.linalg.norm(ref[r0:r0 + p])
+    dY = dev(Y0[c0:c0 + q])
+    ch.hemm_step(1, dH, dev(X[r0:r0 + p]), dY, n, 0.7, -0.3, 0.45)
+    e_b = np.linalg.norm(dY.cpu().numpy() - ref[c0:c0 + q]) / np.linalg.norm(ref[c0:c0 + q])
+    # filter
+    degrees = np.sort(np.array([0, 2, 4, 8, 12, 20, 20, 36] + [20] * 20))
+    V = oracle.random_block(9, 0, N, 0, len(degrees), 0)
+    dV = dev(V[c0:c0 + q])
+    dW = torch.zeros((len(degrees), p), dtype=torch.complex128, device="cuda").t()
+    b_sup, mu_1, mu_ne = M.lam[-1] * 1.01, M.lam[0], M.lam[60]
+    mv = ch.filter(dH, dV, dW, degrees, b_sup, mu_1, mu_ne)
+    fref, _ = oracle.chebyshev_filter(H, V, degrees, b_sup, mu_1, mu_ne)
+    e_filt = np.linalg.norm(dV.cpu().numpy() - fref[c0:c0 + q]) / np.linalg.norm(fref[c0:c0 + q])
+    # full solve
+    vals, dvecs, rep, st = ch.solve(dH, nev, nex, deg=20, tol=1e-10)
+    vecs_local = dvecs.cpu().numpy()[:, :nev]
+    # assemble the V-layout eigenvectors (rows c0..c0+q) from the first row of ranks (i = 0)
+    parts = [None] * world
+    dist.all_gather_object(parts, (r0, p, c0, q, vecs_local, rank % grid[0]))
+    errs = dict(fwd=e_f, bwd=e_b, filter=e_filt)
+    errs = {k: max(v2 for v2 in [v]) for k, v in errs.items()}
+    all_errs = [None] * world
+    dist.all_gather_object(all_errs, (errs, vals.tolist(), st, rep["iterations"]))
+    if rank == 0:
+        normH = np.max(np.abs(M.lam))
+        full = np.zeros((N, nev), dtype=complex)
+        for (rr0, pp, cc0, qq, vl, i) in parts:
+            if i == 0:
+                full[cc0:cc0 + qq] = vl
+        res = np.max(np.linalg.norm(H @ full - full * np.array(vals)[None, :], axis=0)) / normH
+        e_eig = np.max(np.abs(np.array(vals) - M.lam[:nev])) / normH
+        ov, _, orep = oracle.chase_solve(H, nev, nex, deg=20, tol=1e-10)
+        same_vals = all(np.array_equal(np.array(a[1]), np.array(all_errs[0][1])) for a in all_errs)
+        line = {"world": world, "grid": f"{grid[0]}x{grid[1]}", "N": N,
+                "max_step_rel_err": max(max(a[0]["fwd"], a[0]["bwd"]) for a in all_errs),
+                "max_filter_rel_err": max(a[0]["filter"] for a in all_errs),
+                "solve_status": [a[2] for a in all_errs], "iterations": [a[3] for a in all_errs],
+                "oracle_iterations": orep.iterations, "eig_err_rel": e_eig, "resid_rel": res,
+                "eig_vs_oracle": float(np.max(np.abs(np.array(vals) - ov)) / normH),
+                "ritz_identical_on_all_ranks": same_vals,
+                "orth": float(np.max(np.abs(full.conj().T @ full - np.eye(nev))))}
+        ok = (line["max_step_rel_err"] <= 1e-13 and line["max_filter_rel_err"] <= 1e-11 and e_eig <= 1e-10
+              and res <= 1e-10 and all(s == 0 for s in line["solve_status"]) and same_vals and line["orth"] <= 1e-12)
+        line["ok"] = bool(ok)
+        print(json.dumps(line), flush=True)
+    okt = [ok]
+    dist.broadcast_object_list(okt, src=0)
+    ch.close()
+    dist.destroy_process_group()
+    return 0 if okt[0] else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
