@@ -80,7 +80,9 @@ typedef struct {
 chase_status chase_init(chase_handle** out, const chase_init_args* args);
 
 /* Options (defaults): deg_max=36, max_iter=100, lanczos_steps=25, lanczos_runs=4, seed_v=2,
- * seed_lanczos=3, largest=0, approx=0 (1: ritz_vectors holds an initial V-hat on entry). */
+ * seed_lanczos=3, largest=0, approx=0 (1: ritz_vectors holds an initial V-hat on entry),
+ * gemm3m=1 (filter and H*Q products use the 3M complex product -- 3 real DMMAs per complex
+ * multiply-add instead of 4; normwise-stable; 0 selects the 4M kernel). */
 chase_status chase_set_option(chase_handle* h, const char* key, double value);
 
 /* This rank's shard: rows [row0, row0+p) and columns [col0, col0+q) of H. */
@@ -129,6 +131,13 @@ chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t c
 
 chase_status chase_finalize(chase_handle* h);
 const char* chase_last_error(const chase_handle* h);
+
+/* Utility (the Rayleigh-Ritz eigensolver of row a8, exposed for parity tests): Hermitian
+ * eigendecomposition G = Z diag(theta) Z^H of a device n x n matrix (ld) by the library's
+ * block-cyclic Jacobi.  G is destroyed; theta (device, n doubles) ascending; Z device n x n (ldz).
+ * *sweeps (may be NULL) receives the number of outer sweeps.  Local (no communication). */
+chase_status chase_heev(chase_handle* h, void* G, int64_t ld, int32_t n, double* theta, void* Z,
+                        int64_t ldz, int32_t* sweeps);
 
 /* Library build/version string (for diagnostics). */
 const char* chase_version(void);

@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "CHASE_OK", 2: "CHASE_E_USAGE", 3: "CHASE_E_NUMERIC", 4: "CHA
 # exported symbols (include/chase.h); tests check that every one is present
 EXPORTS = ("chase_init", "chase_set_option", "chase_local_layout", "chase_solve", "chase_hemm_step",
            "chase_filter", "chase_lanczos", "chase_random_block", "chase_finalize",
-           "chase_last_error", "chase_version", "chase_nccl_unique_id", "chase_kernel_launches")
+           "chase_last_error", "chase_version", "chase_nccl_unique_id", "chase_kernel_launches", "chase_heev")
 
 
 class ChaseError(RuntimeError):
@@ -72,6 +72,7 @@ def load():
     lib.chase_last_error.restype = C.c_char_p
     lib.chase_version.restype = C.c_char_p
     lib.chase_nccl_unique_id.argtypes = [vp]
+    lib.chase_heev.argtypes = [vp, vp, i64, i32, vp, vp, i64, P(i32)]
     lib.chase_kernel_launches.argtypes = []
     lib.chase_kernel_launches.restype = C.c_ulonglong
     for name in EXPORTS:
@@ -175,6 +176,13 @@ class Chase:
     def random_block(self, V, col0, ncols, seed, stream):
         self._check(self.lib.chase_random_block(self._h, _ptr(V), _ld(V), int(col0), int(ncols),
                                                 C.c_uint64(int(seed)), C.c_uint32(int(stream))))
+
+    def heev(self, G, theta, Z):
+        """Device Hermitian eigensolver (row a8's block Jacobi); G destroyed.  Returns sweeps."""
+        sw = C.c_int32()
+        self._check(self.lib.chase_heev(self._h, _ptr(G), _ld(G), int(G.shape[0]), _ptr(theta), _ptr(Z),
+                                        _ld(Z), C.byref(sw)))
+        return sw.value
 
     def solve(self, H, nev, nex, deg=20, tol=1e-10, vectors=None, report=True):
         import torch

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstring>
 #include "handle.h"
+#include "linalg.h"
 #include "rng.cuh"
 
 using namespace chase;
@@ -62,6 +63,7 @@ void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void*
     d.beta = g.beta_owner_bwd() ? beta : 0.0;
   }
   if (gamma == 0.0 || d.shift_lo >= d.shift_hi) { d.S = nullptr; d.shift_lo = d.shift_hi = 0; }
+  d.use3m = h->opt.gemm3m;
   zgemm(d, h->stream);
   if (dir == 0)
     allreduce_block(h, h->rowc, g.c, Y, p, ldy, ncols);     // row communicator
@@ -299,6 +301,7 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     else if (k == "seed_lanczos") h->opt.seed_lanczos = (uint64_t)v;
     else if (k == "largest") h->opt.largest = v != 0.0;
     else if (k == "approx") h->opt.approx = v != 0.0;
+    else if (k == "gemm3m") h->opt.gemm3m = v != 0.0;
     else throw UsageError("unknown option " + k);
     return CHASE_OK;
   }, false);
@@ -382,6 +385,18 @@ chase_status chase_solve(chase_handle* h, const void* H, int64_t ldh, int64_t N,
     order_after_user(h);
     return solve(h, H, ldh, nev, nex, deg, tol, ritz_values, ritz_vectors, ldv, report);
   });
+}
+
+chase_status chase_heev(chase_handle* h, void* G, int64_t ld, int32_t n, double* theta, void* Z, int64_t ldz,
+                        int32_t* sweeps) {
+  return guarded(h, [&]() {
+    if (!G || !theta || !Z || n <= 0 || ld < n || ldz < n) throw UsageError("bad arguments");
+    order_after_user(h);
+    const int sw = heev_jacobi(G, ld, n, theta, Z, ldz, h->stream);
+    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    if (sweeps) *sweeps = sw;
+    return CHASE_OK;
+  }, false);
 }
 
 chase_status chase_finalize(chase_handle* h) {

@@ -58,6 +58,7 @@ struct Options {
   uint64_t seed_lanczos = 3;
   bool largest = false;
   bool approx = false;
+  bool gemm3m = true;         // 3M complex products in the filter / HQ GEMMs
 };
 
 }  // namespace chase

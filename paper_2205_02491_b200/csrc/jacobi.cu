@@ -11,6 +11,8 @@
 // redundantly on identical inputs gets identical bits (ledger #20).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 #include "common.cuh"
@@ -51,28 +53,29 @@ __global__ void k_pad_init(const double2* G, int64_t ldg, int n, double2* A, dou
 }
 
 // One CTA per pair: diagonalise the 64 x 64 Hermitian subproblem by cyclic Jacobi; write U_k.
-__global__ void __launch_bounds__(256) k_sub_eig(const double2* A, int np, const int* pairs, double2* U) {
+constexpr int SUB_T = 1024;   // 32 rotation pairs x 32 threads
+__global__ void __launch_bounds__(SUB_T) k_sub_eig(const double2* A, int np, const int* pairs, double2* U, int max_inner) {
   extern __shared__ double2 sm[];
   double2* Sm = sm;              // S x LD
   double2* Um = sm + S * LD;     // S x LD
   __shared__ double rc[W], rs[W];
   __shared__ double2 rph[W];
-  __shared__ double red[256];
+  __shared__ double red[SUB_T];
   const int k = blockIdx.x, t = threadIdx.x;
-  for (int idx = t; idx < S * S; idx += 256) {
+  for (int idx = t; idx < S * S; idx += SUB_T) {
     const int i = idx % S, j = idx / S;
     Sm[i * LD + j] = A[gidx(pairs, k, i) + gidx(pairs, k, j) * np];
     Um[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
-  const int pr = t >> 3, sub = t & 7;     // 32 pairs x 8 threads
+  const int pr = t >> 5, sub = t & 31;    // 32 pairs x 32 threads
   __shared__ int nrot;
   if (t == 0) nrot = 0;
   __syncthreads();
-  for (int sweep = 0; sweep < 30; ++sweep) {
+  for (int sweep = 0; sweep < max_inner; ++sweep) {
     // convergence test: off-diagonal Frobenius norm vs total
     double off = 0.0, tot = 0.0;
-    for (int idx = t; idx < S * S; idx += 256) {
+    for (int idx = t; idx < S * S; idx += SUB_T) {
       const int i = idx % S, j = idx / S;
       const double2 v = Sm[i * LD + j];
       const double m2 = v.x * v.x + v.y * v.y;
@@ -81,12 +84,12 @@ __global__ void __launch_bounds__(256) k_sub_eig(const double2* A, int np, const
     }
     red[t] = off;
     __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
+    for (int s = SUB_T / 2; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
     const double offs = red[0];
     __syncthreads();
     red[t] = tot;
     __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
+    for (int s = SUB_T / 2; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
     const double tots = red[0];
     __syncthreads();
     if (offs <= 1e-32 * tots || offs == 0.0) break;
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(256) k_sub_eig(const double2* A, int np, const
       const double c = rc[pr], s = rs[pr];
       const double2 ph = rph[pr];
       // columns:  x_p' = c x_p - s e^{-i phi} x_q ;  x_q' = s x_p + c e^{-i phi} x_q   (S and U)
-      for (int i = sub; i < S; i += 8) {
+      for (int i = sub; i < S; i += 32) {
         {
           const double2 xp = Sm[i * LD + p], xq = cmul(ph, Sm[i * LD + q]);
           Sm[i * LD + p] = make_double2(c * xp.x - s * xq.x, c * xp.y - s * xq.y);
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(256) k_sub_eig(const double2* A, int np, const
       __syncthreads();
       // rows:  y_p' = c y_p - s e^{+i phi} y_q ;  y_q' = s y_p + c e^{+i phi} y_q
       const double2 phc = make_double2(ph.x, -ph.y);
-      for (int j = sub; j < S; j += 8) {
+      for (int j = sub; j < S; j += 32) {
         const double2 yp = Sm[p * LD + j], yq = cmul(phc, Sm[q * LD + j]);
         Sm[p * LD + j] = make_double2(c * yp.x - s * yq.x, c * yp.y - s * yq.y);
         Sm[q * LD + j] = make_double2(s * yp.x + c * yq.x, s * yp.y + c * yq.y);
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(256) k_sub_eig(const double2* A, int np, const
     }
   }
   double2* Uk = U + (int64_t)k * S * S;
-  for (int idx = t; idx < S * S; idx += 256) {
+  for (int idx = t; idx < S * S; idx += SUB_T) {
     const int i = idx % S, j = idx / S;
     Uk[idx] = Um[i * LD + j];          // column-major 64 x 64
   }
@@ -178,9 +181,18 @@ __device__ __forceinline__ void tile_mm(const double2* X, const double2* Y, doub
   }
 }
 
-// A[I_l, I_k] <- U_l^H A[I_l, I_k] U_k for l <= k (and the mirror block for l < k).
-__global__ void __launch_bounds__(256) k_apply_sym(double2* A, int np, const int* pairs, const double2* U, int b) {
+__device__ void apply_z_block(double2* Z, int np, const int* pairs, const double2* U, int rt, int k, double2* sm);
+
+// One launch per round: blocks [0, b(b+1)/2) do A[I_l, I_k] <- U_l^H A[I_l, I_k] U_k for l <= k
+// (and the mirror block for l < k); the remaining (np/64) x b blocks do Z[rows, I_k] <- Z U_k.
+__global__ void __launch_bounds__(256) k_apply(double2* A, double2* Z, int np, const int* pairs, const double2* U, int b) {
   extern __shared__ double2 sm[];
+  const int nsym = b * (b + 1) / 2;
+  if ((int)blockIdx.x >= nsym) {
+    const int e = blockIdx.x - nsym;
+    apply_z_block(Z, np, pairs, U, e % (np / S), e / (np / S), sm);
+    return;
+  }
   double2* Xs = sm;              // S x LD : A block, then T1
   double2* Ys = sm + S * LD;     // S x LD : U_k, then U_l
   // map blockIdx.x -> (l, k), l <= k
@@ -222,11 +234,10 @@ __global__ void __launch_bounds__(256) k_apply_sym(double2* A, int np, const int
 }
 
 // Z[rows rt*64 .. +64, I_k] <- Z[rows, I_k] U_k
-__global__ void __launch_bounds__(256) k_apply_z(double2* Z, int np, const int* pairs, const double2* U) {
-  extern __shared__ double2 sm[];
+__device__ void apply_z_block(double2* Z, int np, const int* pairs, const double2* U, int rt, int k, double2* sm) {
   double2* Xs = sm;
   double2* Ys = sm + S * LD;
-  const int rt = blockIdx.x, k = blockIdx.y, t = threadIdx.x;
+  const int t = threadIdx.x;
   const double2* Uk = U + (int64_t)k * S * S;
   for (int e = t; e < S * S; e += 256) {
     const int i = e % S, j = e / S;
@@ -310,8 +321,7 @@ int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz,
   const int smem = (int)(2 * sizeof(double2) * S * LD);
   if (!attr) {
     CHASE_CUDA(cudaFuncSetAttribute(k_sub_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CHASE_CUDA(cudaFuncSetAttribute(k_apply_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CHASE_CUDA(cudaFuncSetAttribute(k_apply_z, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CHASE_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   // schedule: circle method over 2b blocks, 2b-1 rounds of b pairs
@@ -345,6 +355,11 @@ int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz,
   k_pad_init<<<148 * 8, 256, 0, st>>>(reinterpret_cast<const double2*>(G), ld, n, A, Zp, np, padbase);
   CHASE_CHECK_LAUNCH();
 
+  // Inner sweeps per 64x64 subproblem: exact diagonalisation is wasted effort while the outer
+  // iteration is still in its linear phase; one inner sweep per visit keeps the outer sweep count
+  // (12 at n = 3000, measured) while making each round ~2x cheaper (CHASE_JACOBI_INNER overrides, for experiments).
+  int max_inner = 1;
+  if (const char* e = std::getenv("CHASE_JACOBI_INNER")) max_inner = std::max(1, std::atoi(e));
   int sweeps = 0;
   bool converged = false;
   for (; sweeps < 40; ++sweeps) {
@@ -354,17 +369,19 @@ int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz,
     CHASE_CUDA(cudaStreamSynchronize(st));
     double off = 0.0, t2 = 0.0;
     for (int j = 0; j < np; ++j) { off += part[2 * j]; t2 += part[2 * j + 1]; }
-    // off(A)_F <= 1e-14 ||A||_F (A = padded G; unitarily invariant)
-    if (off <= 1e-28 * t2) { converged = true; break; }
-    if (sweeps >= 12 && off <= 1e-24 * t2) { converged = true; break; }   // rounding floor reached
+    // off(A)_F <= max(1e-14, 4 n u) ||A||_F (A = padded G, unitarily invariant): the in-place
+    // tile updates re-inject O(u ||A||) rounding into every off-diagonal entry, so off_F has a
+    // floor ~ n u ||A||_F; asking for less only burns sweeps.
+    const double tol_rel = std::max(1e-14, 4.0 * np * 1.1102230246251565e-16);
+    if (std::getenv("CHASE_DEBUG_JACOBI"))
+      std::fprintf(stderr, "[jacobi] n=%d sweep=%d off/||A||_F=%.3e tol=%.3e\n", n, sweeps, std::sqrt(off / t2), tol_rel);
+    if (off <= tol_rel * tol_rel * t2) { converged = true; break; }
     for (int r = 0; r < rounds; ++r) {
       const int* pr = g_work.pairs + 2 * (size_t)r * b;
       double2* U = reinterpret_cast<double2*>(g_work.U);
-      k_sub_eig<<<b, 256, smem, st>>>(A, np, pr, U);
+      k_sub_eig<<<b, SUB_T, smem, st>>>(A, np, pr, U, max_inner);
       CHASE_CHECK_LAUNCH();
-      k_apply_sym<<<b * (b + 1) / 2, 256, smem, st>>>(A, np, pr, U, b);
-      CHASE_CHECK_LAUNCH();
-      k_apply_z<<<dim3(np / S, b), 256, smem, st>>>(Zp, np, pr, U);
+      k_apply<<<b * (b + 1) / 2 + (np / S) * b, 256, smem, st>>>(A, Zp, np, pr, U, b);
       CHASE_CHECK_LAUNCH();
     }
   }

@@ -142,6 +142,7 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
   double* alpha_hist = hc + 2 * L * (m + 1);                                        // (m+1) x L x 2
   double* beta_hist = alpha_hist + 2 * (size_t)L * (m + 1);                         // (m+1) x L x 2
 
+  h->scratch.alloc(skinny_work_bytes((int)g.rows.len, (int)g.cols.len, std::min(L, 8)) + 256);
   auto dots_into = [&](const double2* X, int nk, const double2* Y, double* out) {
     const int ncols = nk * L;
     k_proj_p1<<<dim3(ncols, chunks), 256, 0, st>>>(X, N, L, nk, Y, chunks, part);
@@ -161,13 +162,19 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
     double2* Qj = Q + (size_t)j * N * L;
     // F = H Q_j  (rows of block i from this shard; world sum assembles the full vectors)
     CHASE_CUDA(cudaMemsetAsync(F, 0, fbytes, st));
-    ZgemmDesc d;
-    d.M = (int)g.rows.len; d.N = L; d.K = (int)g.cols.len;
-    d.A = H; d.lda = ldh;
-    d.B = Qj + g.cols.start; d.ldb = N;
-    d.C = F + g.rows.start; d.ldc = N;
-    d.alpha = hsign; d.beta = 0.0;
-    zgemm(d, st);
+    if (L == 1 || L == 2 || L == 3 || L == 4 || L == 8) {
+      // HBM-bound skinny product: streams the shard once per step
+      zgemm_skinny((int)g.rows.len, L, (int)g.cols.len, hsign, H, ldh, Qj + g.cols.start, N,
+                   F + g.rows.start, N, h->scratch.p, st);
+    } else {
+      ZgemmDesc d;
+      d.M = (int)g.rows.len; d.N = L; d.K = (int)g.cols.len;
+      d.A = H; d.lda = ldh;
+      d.B = Qj + g.cols.start; d.ldb = N;
+      d.C = F + g.rows.start; d.ldc = N;
+      d.alpha = hsign; d.beta = 0.0;
+      zgemm(d, st);
+    }
     allreduce_doubles(h, h->world, h->world_size, reinterpret_cast<double*>(F), 2 * (size_t)N * L);
     // two classical Gram-Schmidt passes against Q_0..Q_j (full reorthogonalisation); the first
     // pass's coefficient on Q_j is alpha_j = Re(q_j^H H q_j)

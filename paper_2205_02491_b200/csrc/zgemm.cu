@@ -1,6 +1,8 @@
 // Host launcher for the TMA + DMMA complex GEMM (zgemm.cuh) and the tensor-map encoder.
 #include "zgemm.h"
 #include "zgemm.cuh"
+#include "zgemm3m.cuh"
+#include <algorithm>
 
 namespace chase {
 
@@ -57,16 +59,138 @@ static void launch(const ZgemmDesc& d, cudaStream_t st) {
   CHASE_CHECK_LAUNCH();
 }
 
-void zgemm(const ZgemmDesc& d, cudaStream_t st) {
-  if (d.M <= 0 || d.N <= 0) return;
-  if (d.K <= 0) throw CudaError("zgemm: K must be > 0");
-  if (!d.S) {
-    ZgemmDesc e = d;
-    e.shift_lo = e.shift_hi = 0;
-    if (d.conjA) launch<128, 64, true>(e, st); else launch<128, 64, false>(e, st);
+template <bool CONJ>
+static void launch3m(const ZgemmDesc& d, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  if (!CONJ)
+    make_zmatrix_tmap(&ta, d.A, d.M, d.K, d.lda, z3::BK);
+  else
+    make_zmatrix_tmap(&ta, d.A, d.K, d.M, d.lda, z3::BM);
+  make_zmatrix_tmap(&tb, d.B, d.K, d.N, d.ldb, z3::BN);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CHASE_CUDA(cudaFuncSetAttribute(zgemm3m_dmma_kernel<CONJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)z3::SMEM));
+    attr_set = true;
+  }
+  ZgemmParams p;
+  p.M = d.M; p.N = d.N; p.K = d.K;
+  p.alpha = d.alpha; p.beta = d.beta; p.gamma = d.gamma;
+  p.S = reinterpret_cast<const double2*>(d.S); p.lds = d.lds;
+  p.shift_lo = d.shift_lo; p.shift_hi = d.shift_hi; p.shift_off = d.shift_off;
+  p.C = reinterpret_cast<double2*>(d.C); p.ldc = d.ldc;
+  const int grid = ceil_div(d.M, z3::BM) * ceil_div(d.N, z3::BN);
+  zgemm3m_dmma_kernel<CONJ><<<grid, z3::THREADS, z3::SMEM, st>>>(ta, tb, p);
+  CHASE_CHECK_LAUNCH();
+}
+
+void zgemm(const ZgemmDesc& d0, cudaStream_t st) {
+  if (d0.M <= 0 || d0.N <= 0) return;
+  if (d0.K <= 0) throw CudaError("zgemm: K must be > 0");
+  ZgemmDesc d = d0;
+  if (!d.S) d.shift_lo = d.shift_hi = 0;
+  if (d.use3m) {
+    if (d.conjA) launch3m<true>(d, st); else launch3m<false>(d, st);
     return;
   }
   if (d.conjA) launch<128, 64, true>(d, st); else launch<128, 64, false>(d, st);
 }
 
+}  // namespace chase
+
+// ------------------------------------------------------------------ skinny (L <= 8) product
+namespace chase {
+namespace {
+constexpr int SK_T = 256;      // rows per CTA (one per thread)
+constexpr int SK_KB = 128;     // k per shared-memory stage
+
+inline int skinny_splits(int M, int K) {
+  const int rb = ceil_div(M, SK_T);
+  int s = std::max(1, (148 * 8) / std::max(1, rb));
+  s = std::min(s, std::max(1, K / (2 * SK_KB)));
+  return s;
+}
+
+template <int L>
+__global__ void __launch_bounds__(SK_T) k_skinny(int M, int K, int kchunk, const double2* __restrict__ A,
+                                                 int64_t lda, const double2* __restrict__ B, int64_t ldb,
+                                                 double2* __restrict__ P) {
+  __shared__ double2 Bs[SK_KB][L];
+  const int m = blockIdx.x * SK_T + threadIdx.x;
+  const int k0 = blockIdx.y * kchunk, k1 = min(K, k0 + kchunk);
+  double ar[L], ai[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) ar[l] = ai[l] = 0.0;
+  for (int kb = k0; kb < k1; kb += SK_KB) {
+    const int kn = min(SK_KB, k1 - kb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < SK_KB * L; e += SK_T) {
+      const int kk = e % SK_KB, l = e / SK_KB;
+      Bs[kk][l] = kk < kn ? B[(int64_t)(kb + kk) + (int64_t)l * ldb] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    if (m < M) {
+      const double2* a = A + m + (int64_t)kb * lda;
+#pragma unroll 4
+      for (int kk = 0; kk < kn; ++kk) {
+        const double2 h = __ldg(a + (int64_t)kk * lda);
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const double2 b = Bs[kk][l];
+          ar[l] = fma(h.x, b.x, ar[l]);
+          ar[l] = fma(-h.y, b.y, ar[l]);
+          ai[l] = fma(h.x, b.y, ai[l]);
+          ai[l] = fma(h.y, b.x, ai[l]);
+        }
+      }
+    }
+  }
+  if (m < M) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) P[((int64_t)blockIdx.y * L + l) * M + m] = make_double2(ar[l], ai[l]);
+  }
+}
+
+__global__ void k_skinny_reduce(int M, int L, int splits, double alpha, const double2* __restrict__ P,
+                                double2* __restrict__ C, int64_t ldc) {
+  const int64_t total = (int64_t)M * L;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i % M), l = (int)(i / M);
+    double r = 0.0, im = 0.0;
+    for (int s = 0; s < splits; ++s) {
+      const double2 v = P[((int64_t)s * L + l) * M + m];
+      r += v.x;
+      im += v.y;
+    }
+    C[m + (int64_t)l * ldc] = make_double2(alpha * r, alpha * im);
+  }
+}
+}  // namespace
+
+size_t skinny_work_bytes(int M, int K, int L) { return 16 * (size_t)skinny_splits(M, K) * L * M; }
+
+void zgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
+                  void* C, int64_t ldc, void* work, cudaStream_t st) {
+  if (M <= 0 || L <= 0) return;
+  if (L > 8) throw CudaError("zgemm_skinny: L must be <= 8");
+  const int splits = skinny_splits(M, K);
+  const int kchunk = ceil_div(K, splits);
+  dim3 grid(ceil_div(M, SK_T), splits);
+  auto* Ad = reinterpret_cast<const double2*>(A);
+  auto* Bd = reinterpret_cast<const double2*>(B);
+  auto* P = reinterpret_cast<double2*>(work);
+  switch (L) {
+    case 1: k_skinny<1><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 2: k_skinny<2><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 3: k_skinny<3><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 4: k_skinny<4><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 8: k_skinny<8><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    default: throw CudaError("zgemm_skinny: L must be 1, 2, 3, 4 or 8");
+  }
+  CHASE_CHECK_LAUNCH();
+  const int64_t total = (int64_t)M * L;
+  k_skinny_reduce<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(
+      M, L, splits, alpha, P, reinterpret_cast<double2*>(C), ldc);
+  CHASE_CHECK_LAUNCH();
+}
 }  // namespace chase

@@ -74,9 +74,18 @@ __global__ void __launch_bounds__(zg::Cfg<BM, BN>::THREADS, 1)
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grouped rasterisation: a wave of 148 CTAs covers ~8 m-tiles x ~18 n-tiles, so concurrently
+  // resident CTAs share both A row-panels and B column-panels in L2
   const int tiles_n = (p.N + BN - 1) / BN;
-  const int m0 = (blockIdx.x / tiles_n) * BM;
-  const int n0 = (blockIdx.x % tiles_n) * BN;
+  const int tiles_m = (p.M + BM - 1) / BM;
+  constexpr int GROUP_M = 8;
+  const int per_group = GROUP_M * tiles_n;
+  const int group = blockIdx.x / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(tiles_m - first_m, GROUP_M);
+  const int in_group = blockIdx.x % per_group;
+  const int m0 = (first_m + in_group % gsize) * BM;
+  const int n0 = (in_group / gsize) * BN;
   const int KT = (p.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {

@@ -14,9 +14,18 @@ struct ZgemmDesc {
   double alpha = 1.0, beta = 0.0, gamma = 0.0;
   const void* S = nullptr; int64_t lds = 0;   // shift source (may be null)
   int shift_lo = 0, shift_hi = 0; int64_t shift_off = 0;
+  bool use3m = false;            // 3M (Gauss) complex product: 3 real DMMAs per complex MAC
 };
 
 // C = alpha*op(A)*B - alpha*gamma*S[shift rows] + beta*C   (all complex double, column-major)
 void zgemm(const ZgemmDesc& d, cudaStream_t st);
 
+}  // namespace chase
+
+namespace chase {
+// Skinny product C[M x L] = alpha * A[M x K] * B[K x L] for L <= 8 (HBM-bound: streams A once;
+// used by the Lanczos step).  `work` must hold skinny_work_bytes(M, K, L).
+size_t skinny_work_bytes(int M, int K, int L);
+void zgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B,
+                  int64_t ldb, void* C, int64_t ldc, void* work, cudaStream_t st);
 }  // namespace chase

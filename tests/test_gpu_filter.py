@@ -158,3 +158,41 @@ def test_generator_device_twin_bitwise():
     dg.fill(out, 100, 150)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), M.block(100, 200, 150, 300))
+
+
+@pytest.mark.parametrize("N,ncols", [(1000, 75), (333, 7), (257, 130), (1500, 200)])
+@pytest.mark.parametrize("direction", [0, 1])
+@pytest.mark.parametrize("algo", [0, 1])
+def test_hemm_step_3m_and_4m(lib, N, ncols, direction, algo):
+    """Both complex-product kernels (4M: algo 0, 3M Gauss: algo 1) of the fused step: 1e-13 bar."""
+    M = make_matrix("uniform", N, "g2", seed=N + 1)
+    H = M.dense()
+    rng = np.random.default_rng(N + 2 * ncols)
+    X = rng.standard_normal((N, ncols)) + 1j * rng.standard_normal((N, ncols))
+    Y0 = rng.standard_normal((N, ncols)) + 1j * rng.standard_normal((N, ncols))
+    ch = lib.Chase(N, 1, 1)
+    ch.set_option("gemm3m", algo)
+    dH, dX, dY = _dev(H), _dev(X), _dev(Y0)
+    ch.hemm_step(direction, dH, dX, dY, ncols, 0.37, -0.81, 0.55)
+    ref = oracle.hemm_step(H, X, Y0, 0.37, -0.81, 0.55)
+    assert _rel(_host(dY), ref) <= 1e-13
+    ch.close()
+
+
+def test_filter_3m_vs_oracle(lib):
+    N = 900
+    M = make_matrix("wilkinson", N, "g2", seed=8)
+    H = M.dense()
+    degrees = np.sort(np.array([0, 2, 4, 8, 14, 20, 20, 36] + [20] * 40))
+    n = len(degrees)
+    V = np.random.default_rng(3).standard_normal((N, n)) + 0j
+    b_sup, mu_1, mu_ne = M.lam[-1] * 1.02, M.lam[0], M.lam[n]
+    ch = lib.Chase(N, n - 5, 5)
+    ch.set_option("gemm3m", 1)
+    dV = _dev(V)
+    dW = torch.zeros((n, N), dtype=torch.complex128, device="cuda").t()
+    ch.filter(_dev(H), dV, dW, degrees, b_sup, mu_1, mu_ne)
+    ref, _ = oracle.chebyshev_filter(H, V, degrees, b_sup, mu_1, mu_ne)
+    out = _host(dV)
+    for a in range(n):
+        assert _rel(out[:, a], ref[:, a]) <= 1e-11, (a, degrees[a])
