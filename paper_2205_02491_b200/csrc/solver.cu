@@ -125,11 +125,13 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     t_qr.start(st);
     for (int pass = 0; pass < 2 && locked > 0; ++pass) {
       ZgemmDesc d;                                  // T = Y^H Va   (locked x n_act)
+      d.use3m = h->opt.gemm3m;
       d.M = locked; d.N = n_act; d.K = (int)q; d.conjA = true;
       d.A = V; d.lda = q; d.B = Va; d.ldb = q; d.C = G2; d.ldc = locked;
       zgemm(d, st);
       allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G2), 2 * (size_t)locked * n_act);
       ZgemmDesc e;                                  // Va -= Y T
+      e.use3m = h->opt.gemm3m;
       e.M = (int)q; e.N = n_act; e.K = locked;
       e.A = V; e.lda = q; e.B = G2; e.ldb = locked; e.C = Va; e.ldc = q;
       e.alpha = -1.0; e.beta = 1.0;
@@ -139,6 +141,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     for (int pass = 0; pass < cholqr_passes; ++pass) {
       auto gram = [&]() {
         ZgemmDesc d;                                // G = Va^H Va
+        d.use3m = h->opt.gemm3m;
         d.M = n_act; d.N = n_act; d.K = (int)q; d.conjA = true;
         d.A = Va; d.lda = q; d.B = Va; d.ldb = q; d.C = G; d.ldc = n_act;
         zgemm(d, st);
@@ -163,6 +166,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
       }
       trinv_upper(G, n_act, G2, n_act, Z, n_act, st);
       ZgemmDesc d;                                  // V2 = Va R^{-1}
+      d.use3m = h->opt.gemm3m;
       d.M = (int)q; d.N = n_act; d.K = n_act;
       d.A = Va; d.lda = q; d.B = G2; d.ldb = n_act; d.C = V2; d.ldc = q;
       zgemm(d, st);
@@ -175,6 +179,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     hemm_step(h, 0, Hv, ldh, Va, q, HVa, p, n_act, 1.0, 0.0, 0.0);      // HQ (W-layout)
     if (I.len > 0) {
       ZgemmDesc d;                                  // G = Q[I]^H HQ[I]
+      d.use3m = h->opt.gemm3m;
       d.M = n_act; d.N = n_act; d.K = (int)I.len; d.conjA = true;
       d.A = Va + (I.start - c0); d.lda = q;
       d.B = HVa + (I.start - r0); d.ldb = p;
@@ -188,11 +193,13 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     heev_jacobi(G, n_act, n_act, d_theta, Z, n_act, st);
     {
       ZgemmDesc d;                                  // V <- Q Z
+      d.use3m = h->opt.gemm3m;
       d.M = (int)q; d.N = n_act; d.K = n_act;
       d.A = Va; d.lda = q; d.B = Z; d.ldb = n_act; d.C = V2; d.ldc = q;
       zgemm(d, st);
       zcopy2d(Va, q, V2, q, q, n_act, st);
       ZgemmDesc e;                                  // HV <- (HQ) Z   (into W, then swap roles)
+      e.use3m = h->opt.gemm3m;
       e.M = (int)p; e.N = n_act; e.K = n_act;
       e.A = HVa; e.lda = p; e.B = Z; e.ldb = n_act; e.C = Wa; e.ldc = p;
       zgemm(e, st);

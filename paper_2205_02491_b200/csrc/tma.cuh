@@ -60,6 +60,15 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------- host side
 // 2-D FP64 tensor map over a column-major complex matrix (rows x cols, leading dim ld in complex
 // elements).  Dim 0 = 2*rows doubles (contiguous), dim 1 = cols.  Box = {16 doubles (8 complex,
@@ -67,5 +76,11 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
 // (row index mod 8).  Out-of-bounds elements are zero-filled.
 void make_zmatrix_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
                        int box_cols);
+// 3-D view of the same matrix for "row-chunked" tiles (rows % 8 == 0): dim 0 = 16 doubles (8
+// complex rows of a chunk), dim 1 = cols (stride ld), dim 2 = rows/8 chunks (stride 128 B).  One
+// box {16, box_cols, box_chunks} lands as smem [chunk][col][8 rows] -- the forward-A layout -- in a
+// single TMA instead of box_chunks 2-D loads.  Returns false if the driver rejects the map.
+bool make_zmatrix_tmap_chunked(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                               int box_cols, int box_chunks);
 
 }  // namespace chase

@@ -33,14 +33,30 @@ void make_zmatrix_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t
                     std::to_string(rows) + " cols=" + std::to_string(cols) + " ld=" + std::to_string(ld));
 }
 
+bool make_zmatrix_tmap_chunked(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                               int box_cols, int box_chunks) {
+  if (rows % 8 != 0) return false;
+  cuuint64_t dims[3] = {16u, (cuuint64_t)cols, (cuuint64_t)(rows / 8)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 16), 128u};
+  cuuint32_t box[3] = {16u, (cuuint32_t)box_cols, (cuuint32_t)box_chunks};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = get_encode()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int BM, int BN, bool CONJ>
 static void launch(const ZgemmDesc& d, cudaStream_t st) {
   using C_ = zg::Cfg<BM, BN>;
   CUtensorMap ta, tb;
-  if (!CONJ)
-    make_zmatrix_tmap(&ta, d.A, d.M, d.K, d.lda, zg::BK);      // A: M x K
-  else
+  bool chunked = false;
+  if (!CONJ) {
+    chunked = make_zmatrix_tmap_chunked(&ta, d.A, d.M, d.K, d.lda, zg::BK, BM / 8);
+    if (!chunked) make_zmatrix_tmap(&ta, d.A, d.M, d.K, d.lda, zg::BK);      // A: M x K
+  } else {
     make_zmatrix_tmap(&ta, d.A, d.K, d.M, d.lda, BM);          // A: K x M (op = A^H)
+  }
   make_zmatrix_tmap(&tb, d.B, d.K, d.N, d.ldb, BN);
   static bool attr_set = false;
   if (!attr_set) {
@@ -54,23 +70,27 @@ static void launch(const ZgemmDesc& d, cudaStream_t st) {
   p.S = reinterpret_cast<const double2*>(d.S); p.lds = d.lds;
   p.shift_lo = d.shift_lo; p.shift_hi = d.shift_hi; p.shift_off = d.shift_off;
   p.C = reinterpret_cast<double2*>(d.C); p.ldc = d.ldc;
+  p.a_chunked = chunked ? 1 : 0;
   const int grid = ceil_div(d.M, BM) * ceil_div(d.N, BN);
   zgemm_dmma_kernel<BM, BN, CONJ><<<grid, C_::THREADS, C_::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();
 }
 
-template <bool CONJ>
+template <class CFG, bool CONJ>
 static void launch3m(const ZgemmDesc& d, cudaStream_t st) {
   CUtensorMap ta, tb;
-  if (!CONJ)
-    make_zmatrix_tmap(&ta, d.A, d.M, d.K, d.lda, z3::BK);
-  else
-    make_zmatrix_tmap(&ta, d.A, d.K, d.M, d.lda, z3::BM);
-  make_zmatrix_tmap(&tb, d.B, d.K, d.N, d.ldb, z3::BN);
+  bool chunked = false;
+  if (!CONJ) {
+    chunked = make_zmatrix_tmap_chunked(&ta, d.A, d.M, d.K, d.lda, CFG::BK, CFG::BM / 8);
+    if (!chunked) make_zmatrix_tmap(&ta, d.A, d.M, d.K, d.lda, CFG::BK);
+  } else {
+    make_zmatrix_tmap(&ta, d.A, d.K, d.M, d.lda, CFG::BM);
+  }
+  make_zmatrix_tmap(&tb, d.B, d.K, d.N, d.ldb, CFG::BN);
   static bool attr_set = false;
   if (!attr_set) {
-    CHASE_CUDA(cudaFuncSetAttribute(zgemm3m_dmma_kernel<CONJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)z3::SMEM));
+    CHASE_CUDA(cudaFuncSetAttribute(zgemm3m_dmma_kernel<CFG, CONJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)CFG::SMEM));
     attr_set = true;
   }
   ZgemmParams p;
@@ -79,8 +99,9 @@ static void launch3m(const ZgemmDesc& d, cudaStream_t st) {
   p.S = reinterpret_cast<const double2*>(d.S); p.lds = d.lds;
   p.shift_lo = d.shift_lo; p.shift_hi = d.shift_hi; p.shift_off = d.shift_off;
   p.C = reinterpret_cast<double2*>(d.C); p.ldc = d.ldc;
-  const int grid = ceil_div(d.M, z3::BM) * ceil_div(d.N, z3::BN);
-  zgemm3m_dmma_kernel<CONJ><<<grid, z3::THREADS, z3::SMEM, st>>>(ta, tb, p);
+  p.a_chunked = chunked ? 1 : 0;
+  const int grid = ceil_div(d.M, CFG::BM) * ceil_div(d.N, CFG::BN);
+  zgemm3m_dmma_kernel<CFG, CONJ><<<grid, CFG::THREADS, CFG::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();
 }
 
@@ -90,7 +111,7 @@ void zgemm(const ZgemmDesc& d0, cudaStream_t st) {
   ZgemmDesc d = d0;
   if (!d.S) d.shift_lo = d.shift_hi = 0;
   if (d.use3m) {
-    if (d.conjA) launch3m<true>(d, st); else launch3m<false>(d, st);
+    if (d.conjA) launch3m<Z3Default, true>(d, st); else launch3m<Z3Default, false>(d, st);
     return;
   }
   if (d.conjA) launch<128, 64, true>(d, st); else launch<128, 64, false>(d, st);

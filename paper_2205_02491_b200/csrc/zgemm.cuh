@@ -32,6 +32,7 @@ struct ZgemmParams {
   int64_t shift_off;
   double2* C;
   int64_t ldc;
+  int a_chunked;        // forward A loaded by one 3-D TMA box (M % 8 == 0) instead of BM/8 2-D boxes
 };
 
 namespace zg {
@@ -48,15 +49,18 @@ struct Cfg {
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 2 * STAGES * 8 + 1024;
 };
 
+// Not volatile: the compiler may interleave the DMMAs of one k4 step with the fragment loads of
+// the next (software pipelining).  The shared-memory load carries a "memory" clobber so it stays
+// ordered after the mbarrier wait that publishes the TMA data.
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
 __device__ __forceinline__ double2 lds128(uint32_t addr) {
   double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
   return v;
 }
 }  // namespace zg
@@ -106,10 +110,14 @@ __global__ void __launch_bounds__(zg::Cfg<BM, BN>::THREADS, 1)
     mbar_arrive_expect_tx(full + s, C_::STAGE_BYTES);
     const int k0 = kt * BK;
     if constexpr (!CONJ_A) {
-      // A col-major M x K: one box per 8-row chunk -> smem [BM/8][BK][8 m]
+      // A col-major M x K -> smem [BM/8][BK][8 m]: one 3-D box, or one 2-D box per 8-row chunk
+      if (p.a_chunked) {
+        tma_load_3d(sa, &tmA, 0, k0, m0 / 8, full + s);
+      } else {
 #pragma unroll
-      for (int c = 0; c < BM / 8; ++c)
-        tma_load_2d(sa + c * (BK * 128), &tmA, 2 * (m0 + 8 * c), k0, full + s);
+        for (int c = 0; c < BM / 8; ++c)
+          tma_load_2d(sa + c * (BK * 128), &tmA, 2 * (m0 + 8 * c), k0, full + s);
+      }
     } else {
       // A col-major K x M, op = A^H -> smem [BK/8][BM][8 k]
 #pragma unroll

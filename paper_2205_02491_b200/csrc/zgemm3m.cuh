@@ -7,9 +7,9 @@
 // flops.  3M is normwise backward stable (|error| <= c u ||A|| ||B||) but not componentwise; the
 // parity tests hold it to the same 1e-13 relative Frobenius bar as 4M.
 //
-// Tiling: CTA 64 x 64 complex, 8 warps of 32 (m) x 16 (n); three accumulator sets = 96 registers
-// per thread.  6-stage TMA ring of 32 KB stages (SWIZZLE_128B, same conflict-free fragment
-// addressing and k-permutation as zgemm.cuh).
+// Tiling: warps of 32 (m) x 16 (n) complex with three accumulator sets (96 registers per thread);
+// default CTA 96 x 64 with 12 warps (3 per SM sub-partition) and a 5-stage TMA ring of 40 KB stages
+// (SWIZZLE_128B, same conflict-free fragment addressing and k-permutation as zgemm.cuh).
 #pragma once
 #include "common.cuh"
 #include "tma.cuh"
@@ -17,18 +17,25 @@
 
 namespace chase {
 
-namespace z3 {
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 6;
-constexpr int WM = 2, WN = 4, NWARPS = WM * WN, THREADS = NWARPS * 32;
-constexpr uint32_t A_BYTES = BM * BK * 16, B_BYTES = BK * BN * 16, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 2 * STAGES * 8 + 1024;
-}  // namespace z3
+template <int WM_, int WN_, int STAGES_>
+struct Z3Cfg {
+  static constexpr int WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BM = 32 * WM, BN = 16 * WN, BK = 16;
+  static constexpr int NWARPS = WM * WN, THREADS = NWARPS * 32;
+  static constexpr uint32_t A_BYTES = BM * BK * 16, B_BYTES = BK * BN * 16, STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+};
+// default: 12 warps (3 per SM sub-partition) on a 96 x 64 CTA tile, 5 stages of 40 KB
+using Z3Default = Z3Cfg<3, 4, 5>;
 
-template <bool CONJ_A>
-__global__ void __launch_bounds__(z3::THREADS, 1)
+template <class CFG, bool CONJ_A>
+__global__ void __launch_bounds__(CFG::THREADS, 1)
     zgemm3m_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, ZgemmParams p) {
-  using namespace z3;
+  constexpr int WM = CFG::WM, WN = CFG::WN, STAGES = CFG::STAGES, BM = CFG::BM, BN = CFG::BN, BK = CFG::BK;
+  constexpr int NWARPS = CFG::NWARPS;
+  constexpr uint32_t A_BYTES = CFG::A_BYTES, STAGE_BYTES = CFG::STAGE_BYTES;
+  (void)WM;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -64,9 +71,13 @@ __global__ void __launch_bounds__(z3::THREADS, 1)
     mbar_arrive_expect_tx(full + s, STAGE_BYTES);
     const int k0 = kt * BK;
     if constexpr (!CONJ_A) {
+      if (p.a_chunked) {
+        tma_load_3d(sa, &tmA, 0, k0, m0 / 8, full + s);
+      } else {
 #pragma unroll
-      for (int c = 0; c < BM / 8; ++c)
-        tma_load_2d(sa + c * (BK * 128), &tmA, 2 * (m0 + 8 * c), k0, full + s);
+        for (int c = 0; c < BM / 8; ++c)
+          tma_load_2d(sa + c * (BK * 128), &tmA, 2 * (m0 + 8 * c), k0, full + s);
+      }
     } else {
 #pragma unroll
       for (int kc = 0; kc < BK / 8; ++kc)

@@ -16,8 +16,7 @@ dg.fill(H, 0, 0)
 V = torch.randn((n, N), dtype=torch.complex128, device="cuda").t()
 W = torch.zeros((n, N), dtype=torch.complex128, device="cuda").t()
 ch = pkg.Chase(N, n - 10, 10)
-if len(sys.argv) > 3 and sys.argv[3] == "3m":
-    ch.set_option("gemm3m", 1)
+ch.set_option("gemm3m", 1 if (len(sys.argv) <= 3 or sys.argv[3] == "3m") else 0)
 for d in (0, 1):
     ch.hemm_step(d, H, V if d == 0 else W, W if d == 0 else V, n, 1e-3, 0.5, 0.3)
 torch.cuda.synchronize()
@@ -28,4 +27,4 @@ for d in (0, 1):
         ch.hemm_step(d, H, V if d == 0 else W, W if d == 0 else V, n, 1e-3, 0.5, 0.3)
         ts.append(time.perf_counter() - t)
     flops = 8.0 * N * N * n
-    print(json.dumps({"algo": sys.argv[3] if len(sys.argv) > 3 else "4m", "dir": d, "N": N, "n": n, "s": min(ts), "tflops": flops / min(ts) / 1e12}))
+    print(json.dumps({"algo": sys.argv[3] if len(sys.argv) > 3 else "3m", "dir": d, "N": N, "n": n, "s": min(ts), "tflops": flops / min(ts) / 1e12}))
