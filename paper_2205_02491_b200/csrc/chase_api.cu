@@ -1,7 +1,9 @@
 // C ABI of the ChASE B200 library + the filter driver.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 #include "handle.h"
 #include "linalg.h"
 #include "rng.cuh"
@@ -34,9 +36,9 @@ void allreduce_doubles(chase_handle* h, ncclComm_t comm, int comm_size, double* 
 }
 
 // ------------------------------------------------------------------- fused recurrence step
-void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
-               void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma) {
-  if (ncols <= 0) return;
+// Local part of one distributed step (a2 / a4): the GEMM descriptor for this rank's shard.
+static ZgemmDesc step_desc(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
+                           void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma) {
   const Grid& g = h->grid;
   const int64_t r0 = g.rows.start, p = g.rows.len, c0 = g.cols.start, q = g.cols.len;
   ZgemmDesc d;
@@ -64,11 +66,18 @@ void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void*
   }
   if (gamma == 0.0 || d.shift_lo >= d.shift_hi) { d.S = nullptr; d.shift_lo = d.shift_hi = 0; }
   d.use3m = h->opt.gemm3m;
-  zgemm(d, h->stream);
+  return d;
+}
+
+void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
+               void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma) {
+  if (ncols <= 0) return;
+  const Grid& g = h->grid;
+  zgemm(step_desc(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma), h->stream);
   if (dir == 0)
-    allreduce_block(h, h->rowc, g.c, Y, p, ldy, ncols);     // row communicator
+    allreduce_block(h, h->rowc, g.c, Y, g.rows.len, ldy, ncols);     // row communicator
   else
-    allreduce_block(h, h->colc, g.r, Y, q, ldy, ncols);     // column communicator
+    allreduce_block(h, h->colc, g.r, Y, g.cols.len, ldy, ncols);     // column communicator
 }
 
 // ------------------------------------------------------------------------ Chebyshev filter
@@ -94,10 +103,23 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
   double sigma_prev = sigma1;
   double2* Vz = reinterpret_cast<double2*>(V);
   double2* Wz = reinterpret_cast<double2*>(W);
+  const Grid& g = h->grid;
+  // Overlap: on a real grid the columns are cut into chunks with fixed absolute
+  // boundaries; each chunk's all-reduce runs on the comm stream while the next chunk's GEMM runs,
+  // and step k's GEMM on chunk c waits only for step k-1's all-reduce of chunk c (columns are
+  // independent through the whole recurrence).
+  const bool comm = h->comm_stream && (g.r > 1 || g.c > 1) && h->world;
+  int nchunks = comm ? std::max(1, std::min(chase_handle::MAX_CHUNKS, ncols / 384)) : 1;
+  if (comm) {
+    if (const char* env = std::getenv("CHASE_FILTER_CHUNKS"))      // testing / tuning override
+      nchunks = std::max(1, std::min({chase_handle::MAX_CHUNKS, ncols, std::atoi(env)}));
+  }
+  std::vector<int> bnd(nchunks + 1);
+  for (int c = 0; c <= nchunks; ++c) bnd[c] = (int)((int64_t)ncols * c / nchunks);
+  bool rec[2][chase_handle::MAX_CHUNKS] = {};
   int first = 0;
   for (int k = 1; k <= kmax; ++k) {
     while (first < ncols && degrees[first] < k) ++first;
-    const int nk = ncols - first;
     double alpha, beta;
     if (k == 1) {
       alpha = sigma1 / e;
@@ -108,12 +130,39 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       beta = -sigma_prev * sigma;
       sigma_prev = sigma;
     }
-    if (k & 1)
-      hemm_step(h, 0, H, ldh, Vz + (int64_t)first * ldv, ldv, Wz + (int64_t)first * ldw, ldw, nk,
+    const int dir = (k & 1) ? 0 : 1;        // odd: forward V -> W; even: backward W -> V
+    double2* X = dir == 0 ? Vz : Wz;
+    double2* Y = dir == 0 ? Wz : Vz;
+    const int64_t ldx = dir == 0 ? ldv : ldw, ldy = dir == 0 ? ldw : ldv;
+    if (!comm) {
+      hemm_step(h, dir, H, ldh, X + (int64_t)first * ldx, ldx, Y + (int64_t)first * ldy, ldy, ncols - first,
                 alpha, beta, c);
-    else
-      hemm_step(h, 1, H, ldh, Wz + (int64_t)first * ldw, ldw, Vz + (int64_t)first * ldv, ldv, nk,
-                alpha, beta, c);
+      continue;
+    }
+    const int64_t rows = dir == 0 ? g.rows.len : g.cols.len;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int lo = std::max(first, bnd[ch]), hi = bnd[ch + 1];
+      if (lo >= hi) continue;
+      if (rec[(k - 1) & 1][ch]) CHASE_CUDA(cudaStreamWaitEvent(h->stream, h->ev_comm[(k - 1) & 1][ch], 0));
+      zgemm(step_desc(h, dir, H, ldh, X + (int64_t)lo * ldx, ldx, Y + (int64_t)lo * ldy, ldy, hi - lo, alpha,
+                      beta, c), h->stream);
+      CHASE_CUDA(cudaEventRecord(h->ev_gemm[ch], h->stream));
+      CHASE_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_gemm[ch], 0));
+      cudaStream_t saved = h->stream;
+      h->stream = h->comm_stream;               // allreduce_block enqueues on h->stream
+      if (dir == 0)
+        allreduce_block(h, h->rowc, g.c, Y + (int64_t)lo * ldy, rows, ldy, hi - lo);
+      else
+        allreduce_block(h, h->colc, g.r, Y + (int64_t)lo * ldy, rows, ldy, hi - lo);
+      h->stream = saved;
+      CHASE_CUDA(cudaEventRecord(h->ev_comm[k & 1][ch], h->comm_stream));
+      rec[k & 1][ch] = true;
+      rec[(k - 1) & 1][ch] = false;
+    }
+  }
+  if (comm) {
+    CHASE_CUDA(cudaEventRecord(h->ev_join, h->comm_stream));
+    CHASE_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   }
   return matvecs;
 }
@@ -252,6 +301,13 @@ chase_status chase_init(chase_handle** out, const chase_init_args* a) {
       CHASE_NCCL(ncclCommInitRank(&h->world, ws, id, a->rank));
       CHASE_NCCL(ncclCommSplit(h->world, h->grid.i, h->grid.j, &h->rowc, nullptr));   // row comm i
       CHASE_NCCL(ncclCommSplit(h->world, h->grid.j, h->grid.i, &h->colc, nullptr));   // column comm j
+      CHASE_CUDA(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+      for (int c = 0; c < chase_handle::MAX_CHUNKS; ++c) {
+        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_gemm[c], cudaEventDisableTiming));
+        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_comm[0][c], cudaEventDisableTiming));
+        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_comm[1][c], cudaEventDisableTiming));
+      }
+      CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     }
     h->n_e_max = a->nev_max + a->nex_max;
     // Workspace: V, V2 (V-layout q x n_e), W, HV (W-layout p x n_e), n_e x n_e
@@ -408,6 +464,14 @@ chase_status chase_finalize(chase_handle* h) {
   if (h->rowc) ncclCommDestroy(h->rowc);
   if (h->colc) ncclCommDestroy(h->colc);
   if (h->world) ncclCommDestroy(h->world);
+  if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
+  for (int c = 0; c < chase_handle::MAX_CHUNKS; ++c) {
+    if (h->ev_gemm[c]) cudaEventDestroy(h->ev_gemm[c]);
+    if (h->ev_comm[0][c]) cudaEventDestroy(h->ev_comm[0][c]);
+    if (h->ev_comm[1][c]) cudaEventDestroy(h->ev_comm[1][c]);
+  }
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);

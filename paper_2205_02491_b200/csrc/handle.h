@@ -77,6 +77,10 @@ struct chase_handle {
   std::vector<double> host_scratch;
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // filter pipelining (grid runs): GEMM chunks on `stream`, their all-reduces on `comm_stream`
+  cudaStream_t comm_stream = nullptr;
+  static constexpr int MAX_CHUNKS = 8;
+  cudaEvent_t ev_gemm[MAX_CHUNKS] = {}, ev_comm[2][MAX_CHUNKS] = {}, ev_join = nullptr;
   bool broken = false;
 };
 

@@ -17,6 +17,8 @@
 // by these distributed forms (its future-work item).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 #include "dense.h"
@@ -88,6 +90,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
   int* d_info = d_perm + n_e;
 
   PhaseTimer t_all, t_lz, t_f, t_qr, t_rr, t_res;
+  const bool trace = std::getenv("CHASE_TRACE") != nullptr;   // per-iteration phase trace to stderr
   t_all.start(st);
 
   // ---- Alg. 1 line 2: Lanczos bounds
@@ -217,7 +220,12 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     CHASE_CUDA(cudaMemcpyAsync(th_h.data(), d_theta, sizeof(double) * n_act, cudaMemcpyDeviceToHost, st));
     CHASE_CUDA(cudaMemcpyAsync(r2_h.data(), d_res2, sizeof(double) * n_act, cudaMemcpyDeviceToHost, st));
     CHASE_CUDA(cudaStreamSynchronize(st));
+    const double f0 = t_f.total_ms, q0 = t_qr.total_ms, r0_ = t_rr.total_ms, s0 = t_res.total_ms;
     t_f.collect(); t_qr.collect(); t_rr.collect(); t_res.collect();
+    if (trace && g.rank == 0)
+      std::fprintf(stderr, "[chase] it=%d n_act=%d locked_before=%d matvecs=%lld filter=%.3fs qr=%.3fs rr=%.3fs resid=%.4fs\n",
+                   it, n_act, locked, (long long)matvecs, (t_f.total_ms - f0) * 1e-3, (t_qr.total_ms - q0) * 1e-3,
+                   (t_rr.total_ms - r0_) * 1e-3, (t_res.total_ms - s0) * 1e-3);
     for (int a = 0; a < n_act; ++a) {
       ritz[locked + a] = th_h[a];
       res[locked + a] = std::sqrt(std::max(0.0, r2_h[a])) / nu;
