@@ -17,6 +17,7 @@
 #include <vector>
 #include "common.cuh"
 #include "dense.h"
+#include "tma.cuh"
 #include "handle.h"
 #include "linalg.h"
 
@@ -154,105 +155,177 @@ __global__ void __launch_bounds__(SUB_T) k_sub_eig(const double2* A, int np, con
   }
 }
 
-// 64x64x64 complex tile product in shared memory: out = op(X) * Y, op = identity or ^H.
-// 256 threads; thread (tx, ty) owns rows ty + 16 r, cols tx + 16 c (r, c < 4).
+// ---- 64x64x64 complex tile products on the FP64 tensor cores (DMMA.8x8x4, complex 4M) ------
+// Tiles live in shared memory in the same swizzled "[k-chunk][row][8 k]" layout the filter GEMM
+// uses (16-byte complex elements, chunk index XOR row%8), so every fragment load of the 8 warps is
+// bank-conflict free.  off(r, k): byte offset of element (row r, contraction index k).
+__device__ __forceinline__ uint32_t toff(int r, int k) {
+  return (uint32_t)((((k >> 3) * S + r) << 7) + ((((k & 7) ^ (r & 7))) << 4));
+}
+__device__ __forceinline__ void tst(unsigned char* base, int r, int k, double2 v) {
+  *reinterpret_cast<double2*>(base + toff(r, k)) = v;
+}
+
+__device__ __forceinline__ void dmma_j(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double2 lds_j(uint32_t addr) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+
+// acc = op(X) * Y with X (rows x k) and Y (k x cols) tiles; warp w owns rows 32*(w/4) + [0,32),
+// cols 16*(w%4) + [0,16): acc[mt][nt][{re,im}][j] = C[32 wm + 8 mt + g][16 wn + 8 nt + 2 t + j].
 template <bool CONJX>
-__device__ __forceinline__ void tile_mm(const double2* X, const double2* Y, double2 (&acc)[4][4]) {
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+__device__ __forceinline__ void tile_dmma(uint32_t xs, uint32_t ys, double (&acc)[4][2][2][2]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = w >> 2, wn = w & 3, g = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = make_double2(0.0, 0.0);
+    for (int j = 0; j < 2; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
 #pragma unroll 4
-  for (int m = 0; m < S; ++m) {
-    double2 xv[4], yv[4];
+  for (int ks = 0; ks < S / 4; ++ks) {
+    const int k = (ks >> 1) * 8 + 2 * t + (ks & 1);
+    double2 a[4], b[2];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) xv[r] = CONJX ? X[m * LD + ty + 16 * r] : X[(ty + 16 * r) * LD + m];
+    for (int mt = 0; mt < 4; ++mt) {
+      a[mt] = lds_j(xs + toff(wm * 32 + mt * 8 + g, k));
+      if (CONJX) a[mt].y = -a[mt].y;
+    }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) yv[c] = Y[m * LD + tx + 16 * c];
+    for (int nt = 0; nt < 2; ++nt) b[nt] = lds_j(ys + toff(wn * 16 + nt * 8 + g, k));
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int nt = 0; nt < 2; ++nt) {
+      const double nbi = -b[nt].y;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double2 u = CONJX ? cmulc(xv[r], yv[c]) : cmul(xv[r], yv[c]);
-        acc[r][c].x += u.x;
-        acc[r][c].y += u.y;
+      for (int mt = 0; mt < 4; ++mt) {
+        dmma_j(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].x, b[nt].x);
+        dmma_j(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].x, b[nt].y);
+        dmma_j(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].y, nbi);
+        dmma_j(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].y, b[nt].x);
       }
+    }
   }
 }
 
-__device__ void apply_z_block(double2* Z, int np, const int* pairs, const double2* U, int rt, int k, double2* sm);
+__device__ void apply_z_block(double2* Z, int np, const int* pairs, const double2* U, int rt, int k,
+                              unsigned char* sm);
 
 // One launch per round: blocks [0, b(b+1)/2) do A[I_l, I_k] <- U_l^H A[I_l, I_k] U_k for l <= k
 // (and the mirror block for l < k); the remaining (np/64) x b blocks do Z[rows, I_k] <- Z U_k.
-__global__ void __launch_bounds__(256) k_apply(double2* A, double2* Z, int np, const int* pairs, const double2* U, int b) {
-  extern __shared__ double2 sm[];
+__global__ void __launch_bounds__(256, 1) k_apply(double2* A, double2* Z, int np, const int* pairs,
+                                                  const double2* U, int b) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   const int nsym = b * (b + 1) / 2;
   if ((int)blockIdx.x >= nsym) {
     const int e = blockIdx.x - nsym;
     apply_z_block(Z, np, pairs, U, e % (np / S), e / (np / S), sm);
     return;
   }
-  double2* Xs = sm;              // S x LD : A block, then T1
-  double2* Ys = sm + S * LD;     // S x LD : U_k, then U_l
-  // map blockIdx.x -> (l, k), l <= k
+  unsigned char* Xs = sm;                  // 64 KB: A_lk, then U_l (as U_l^H)
+  unsigned char* Ys = sm + S * S * 16;     // 64 KB: U_k, then T1
   int idx = blockIdx.x, l = 0;
   while (idx >= b - l) { idx -= b - l; ++l; }
   const int k = l + idx;
   const int t = threadIdx.x;
   const double2* Uk = U + (int64_t)k * S * S;
   const double2* Ul = U + (int64_t)l * S * S;
-  for (int e = t; e < S * S; e += 256) {
-    const int i = e % S, j = e / S;
-    Xs[i * LD + j] = A[gidx(pairs, l, i) + gidx(pairs, k, j) * np];
-    Ys[i * LD + j] = Uk[i + j * S];
-  }
-  __syncthreads();
-  double2 acc[4][4];
-  tile_mm<false>(Xs, Ys, acc);                 // T1 = A_lk U_k
-  __syncthreads();
-  const int tx = t & 15, ty = t >> 4;
+  {
+    // batched global loads (16 + 16 independent 16-byte loads in flight per thread), then stores
+    double2 xa[16], ya[16];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) Xs[(ty + 16 * r) * LD + tx + 16 * c] = acc[r][c];
-  for (int e = t; e < S * S; e += 256) {
-    const int i = e % S, j = e / S;
-    Ys[i * LD + j] = Ul[i + j * S];
-  }
-  __syncthreads();
-  tile_mm<true>(Ys, Xs, acc);                  // T = U_l^H T1
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int i = ty + 16 * r, j = tx + 16 * c;
-      const int64_t gi = gidx(pairs, l, i), gj = gidx(pairs, k, j);
-      A[gi + gj * np] = acc[r][c];
-      if (l != k) A[gj + gi * np] = make_double2(acc[r][c].x, -acc[r][c].y);
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + 256 * it, i = e % S, j = e / S;
+      xa[it] = A[gidx(pairs, l, i) + gidx(pairs, k, j) * np];
+      ya[it] = Uk[i + j * S];
     }
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + 256 * it, i = e % S, j = e / S;
+      tst(Xs, i, j, xa[it]);                                         // X[i][k=j]
+      tst(Ys, j, i, ya[it]);                                         // Y[k=i][n=j]
+    }
+  }
+  __syncthreads();
+  double acc[4][2][2][2];
+  tile_dmma<false>(smem_u32(Xs), smem_u32(Ys), acc);                 // T1 = A_lk U_k
+  __syncthreads();
+  const int w = t >> 5, lane = t & 31, wm = w >> 2, wn = w & 3, g = lane >> 2, tt = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)   // T1[row][col] is Y'[k=row][n=col]
+        tst(Ys, wn * 16 + nt * 8 + 2 * tt + j, wm * 32 + mt * 8 + g,
+            make_double2(acc[mt][nt][0][j], acc[mt][nt][1][j]));
+  {
+    double2 ua[16];
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + 256 * it;
+      ua[it] = Ul[e];
+    }
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + 256 * it, kk = e % S, i = e / S;
+      tst(Xs, i, kk, ua[it]);                                        // X'[i][k] = conj(U_l[k][i])
+    }
+  }
+  __syncthreads();
+  tile_dmma<true>(smem_u32(Xs), smem_u32(Ys), acc);                  // T = U_l^H T1
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int i = wm * 32 + mt * 8 + g, jj = wn * 16 + nt * 8 + 2 * tt + j;
+        const int64_t gi = gidx(pairs, l, i), gj = gidx(pairs, k, jj);
+        const double2 v = make_double2(acc[mt][nt][0][j], acc[mt][nt][1][j]);
+        A[gi + gj * np] = v;
+        if (l != k) A[gj + gi * np] = make_double2(v.x, -v.y);
+      }
 }
 
 // Z[rows rt*64 .. +64, I_k] <- Z[rows, I_k] U_k
-__device__ void apply_z_block(double2* Z, int np, const int* pairs, const double2* U, int rt, int k, double2* sm) {
-  double2* Xs = sm;
-  double2* Ys = sm + S * LD;
+__device__ void apply_z_block(double2* Z, int np, const int* pairs, const double2* U, int rt, int k,
+                              unsigned char* sm) {
+  unsigned char* Xs = sm;
+  unsigned char* Ys = sm + S * S * 16;
   const int t = threadIdx.x;
   const double2* Uk = U + (int64_t)k * S * S;
-  for (int e = t; e < S * S; e += 256) {
-    const int i = e % S, j = e / S;
-    Xs[i * LD + j] = Z[(int64_t)(rt * S + i) + gidx(pairs, k, j) * np];
-    Ys[i * LD + j] = Uk[i + j * S];
+  {
+    double2 xa[16], ya[16];
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + 256 * it, i = e % S, j = e / S;
+      xa[it] = Z[(int64_t)(rt * S + i) + gidx(pairs, k, j) * np];
+      ya[it] = Uk[i + j * S];
+    }
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+      const int e = t + 256 * it, i = e % S, j = e / S;
+      tst(Xs, i, j, xa[it]);
+      tst(Ys, j, i, ya[it]);
+    }
   }
   __syncthreads();
-  double2 acc[4][4];
-  tile_mm<false>(Xs, Ys, acc);
-  const int tx = t & 15, ty = t >> 4;
+  double acc[4][2][2][2];
+  tile_dmma<false>(smem_u32(Xs), smem_u32(Ys), acc);
+  const int w = t >> 5, lane = t & 31, wm = w >> 2, wn = w & 3, g = lane >> 2, tt = lane & 3;
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      Z[(int64_t)(rt * S + ty + 16 * r) + gidx(pairs, k, tx + 16 * c) * np] = acc[r][c];
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        Z[(int64_t)(rt * S + wm * 32 + mt * 8 + g) + gidx(pairs, k, wn * 16 + nt * 8 + 2 * tt + j) * np] =
+            make_double2(acc[mt][nt][0][j], acc[mt][nt][1][j]);
 }
 
 // partial sums of |A_ij|^2: off-diagonal and total, per block of rows (fixed order)
@@ -319,9 +392,10 @@ int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz,
   g_work.ensure(np, st);
   static bool attr = false;
   const int smem = (int)(2 * sizeof(double2) * S * LD);
+  const int smem_apply = 2 * S * S * 16 + 1024;
   if (!attr) {
     CHASE_CUDA(cudaFuncSetAttribute(k_sub_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CHASE_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CHASE_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_apply));
     attr = true;
   }
   // schedule: circle method over 2b blocks, 2b-1 rounds of b pairs
@@ -381,7 +455,7 @@ int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz,
       double2* U = reinterpret_cast<double2*>(g_work.U);
       k_sub_eig<<<b, SUB_T, smem, st>>>(A, np, pr, U, max_inner);
       CHASE_CHECK_LAUNCH();
-      k_apply<<<b * (b + 1) / 2 + (np / S) * b, 256, smem, st>>>(A, Zp, np, pr, U, b);
+      k_apply<<<b * (b + 1) / 2 + (np / S) * b, 256, smem_apply, st>>>(A, Zp, np, pr, U, b);
       CHASE_CHECK_LAUNCH();
     }
   }
