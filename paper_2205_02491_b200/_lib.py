@@ -190,6 +190,8 @@ class Chase:
         vals = (C.c_double * nev)()
         if vectors is None:
             vectors = torch.empty((nev + nex, q), dtype=torch.complex128, device=H.device).t()
+        elif vectors.shape[0] != q:
+            raise ValueError("vectors must be V-layout (q rows)")
         rep = Report()
         st = self.lib.chase_solve(self._h, _ptr(H), _ld(H), self.N, int(nev), int(nex), int(deg),
                                   float(tol), vals, _ptr(vectors), _ld(vectors), C.byref(rep))

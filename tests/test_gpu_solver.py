@@ -112,3 +112,27 @@ def test_solve_rejects_bad_arguments(lib):
         ch.solve(H, 20, 5)          # exceeds nev_max + nex_max
     with pytest.raises(lib.ChaseError):
         ch.solve(H, 5, 5, tol=-1.0)
+
+
+def test_warm_start_sequence(lib):
+    """Sequences of correlated eigenproblems: solve H1 cold, then
+    H2 = H1 + small Hermitian perturbation warm-started (approx=1) from H1's Ritz vectors.  The warm
+    solve must match the oracle's cold solve of H2 and need fewer iterations than a cold solve."""
+    N, nev, nex = 600, 40, 20
+    M = make_matrix("uniform", N, "g2", seed=21)
+    H1 = M.dense()
+    rng = np.random.default_rng(5)
+    E = rng.standard_normal((N, N)) + 1j * rng.standard_normal((N, N))
+    H2 = H1 + 1e-5 * (E + E.conj().T) / np.sqrt(N)
+    ch = lib.Chase(N, nev, nex)
+    vec = torch.zeros((nev + nex, N), dtype=torch.complex128, device="cuda").t()
+    v1, vec, r1, st = ch.solve(_dev(H1), nev, nex, vectors=vec)
+    assert st == 0
+    vec[:, nev:] = torch.from_numpy(np.asfortranarray(oracle.random_block(7, 0, N, 0, nex, 0))).cuda()
+    _, _, rc, _ = ch.solve(_dev(H2), nev, nex)                      # cold reference on the device
+    ch.set_option("approx", 1)
+    v2, vec2, rw, st = ch.solve(_dev(H2), nev, nex, vectors=vec)
+    assert st == 0
+    ov, _, _ = oracle.chase_solve(H2, nev, nex)
+    assert np.max(np.abs(v2 - ov)) <= 1e-10 * np.max(np.abs(M.lam)) * 1.01
+    assert rw["iterations"] < rc["iterations"], (rw["iterations"], rc["iterations"])
