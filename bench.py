@@ -137,7 +137,7 @@ def oracle_sample(N, seconds=12.0, rows=1024, ncols=64, family="uniform"):
     return flops / el / 1e12, cores, f"{n} oracle filter steps (hemm_step, P:385-390) on a {rows} x {N} row panel of H times {ncols} columns, numpy complex128"
 
 
-def run_reference(args):
+def run_reference(args, out):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -163,15 +163,24 @@ def run_reference(args):
                        "N": N, "grid": f"{r}x{c}"},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=out, flush=True)
     return 0
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def _json_out():
+    """Keep stdout for the single JSON line: libraries (NCCL's version banner, CUDA) write to fd 1,
+    so fd 1 is pointed at stderr for the run and the result goes to the saved descriptor."""
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(saved, "w")
+
+
 def main():
     args = parse()
+    out = _json_out()
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args, out)
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -315,7 +324,7 @@ def main():
         if world == 1 and not args.no_cpu:
             v, cores, sample = oracle_sample(N, seconds=12.0, family=args.family)
             line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=out, flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

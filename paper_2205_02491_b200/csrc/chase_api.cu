@@ -109,7 +109,13 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
   // and step k's GEMM on chunk c waits only for step k-1's all-reduce of chunk c (columns are
   // independent through the whole recurrence).
   const bool comm = h->comm_stream && (g.r > 1 || g.c > 1) && h->world;
-  int nchunks = comm ? std::max(1, std::min(chase_handle::MAX_CHUNKS, ncols / 384)) : 1;
+  // Chunking costs GEMM tile/wave efficiency (~1-2 % per extra chunk), so it is only worth it when
+  // the all-reduce is a visible fraction of a step: t_comm / t_gemm ~ (16 B/elem / ~600 GB/s) /
+  // (8 K flop/elem / ~40 TF/s) ~ 133 / K.  Measured on B200 (2x2 grid, K = 30000) it is 0.4 %, so
+  // large shards run one GEMM + one all-reduce per step; small-K shards pipeline.
+  const int64_t kmin = std::min(g.rows.len, g.cols.len);
+  int nchunks = (comm && 133.0 / (double)kmin > 0.03)
+                    ? std::max(1, std::min(chase_handle::MAX_CHUNKS, ncols / 384)) : 1;
   if (comm) {
     if (const char* env = std::getenv("CHASE_FILTER_CHUNKS"))      // testing / tuning override
       nchunks = std::max(1, std::min({chase_handle::MAX_CHUNKS, ncols, std::atoi(env)}));
