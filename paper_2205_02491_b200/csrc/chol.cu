@@ -157,6 +157,7 @@ bool cholesky_upper(void* Gv, int64_t ld, int n, int* d_info, cudaStream_t st) {
     d.B = d.A; d.ldb = ld;
     d.C = G + (kb + nb) + (int64_t)(kb + nb) * ld; d.ldc = ld;
     d.alpha = -1.0; d.beta = 1.0;
+    d.upper_only = true;          // only the upper triangle of the trailing matrix is ever read
     zgemm(d, st);
   }
   int info = 0;

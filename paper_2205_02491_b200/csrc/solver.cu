@@ -146,6 +146,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
         ZgemmDesc d;                                // G = Va^H Va
         d.use3m = h->opt.gemm3m;
         d.M = n_act; d.N = n_act; d.K = (int)q; d.conjA = true;
+        d.upper_only = true;                        // Cholesky reads the upper triangle only
         d.A = Va; d.lda = q; d.B = Va; d.ldb = q; d.C = G; d.ldc = n_act;
         zgemm(d, st);
         allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G), 2 * (size_t)n_act * n_act);
@@ -171,6 +172,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
       ZgemmDesc d;                                  // V2 = Va R^{-1}
       d.use3m = h->opt.gemm3m;
       d.M = (int)q; d.N = n_act; d.K = n_act;
+      d.b_upper = true;                             // R^{-1} is upper triangular
       d.A = Va; d.lda = q; d.B = G2; d.ldb = n_act; d.C = V2; d.ldc = q;
       zgemm(d, st);
       zcopy2d(Va, q, V2, q, q, n_act, st);

@@ -71,6 +71,8 @@ static void launch(const ZgemmDesc& d, cudaStream_t st) {
   p.shift_lo = d.shift_lo; p.shift_hi = d.shift_hi; p.shift_off = d.shift_off;
   p.C = reinterpret_cast<double2*>(d.C); p.ldc = d.ldc;
   p.a_chunked = chunked ? 1 : 0;
+  p.upper_only = d.upper_only ? 1 : 0;
+  p.b_upper = d.b_upper ? 1 : 0;
   const int grid = ceil_div(d.M, BM) * ceil_div(d.N, BN);
   zgemm_dmma_kernel<BM, BN, CONJ><<<grid, C_::THREADS, C_::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();
@@ -100,6 +102,8 @@ static void launch3m(const ZgemmDesc& d, cudaStream_t st) {
   p.shift_lo = d.shift_lo; p.shift_hi = d.shift_hi; p.shift_off = d.shift_off;
   p.C = reinterpret_cast<double2*>(d.C); p.ldc = d.ldc;
   p.a_chunked = chunked ? 1 : 0;
+  p.upper_only = d.upper_only ? 1 : 0;
+  p.b_upper = d.b_upper ? 1 : 0;
   const int grid = ceil_div(d.M, CFG::BM) * ceil_div(d.N, CFG::BN);
   zgemm3m_dmma_kernel<CFG, CONJ><<<grid, CFG::THREADS, CFG::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();

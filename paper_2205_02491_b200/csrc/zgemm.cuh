@@ -33,6 +33,8 @@ struct ZgemmParams {
   double2* C;
   int64_t ldc;
   int a_chunked;        // forward A loaded by one 3-D TMA box (M % 8 == 0) instead of BM/8 2-D boxes
+  int upper_only;       // skip output tiles strictly below the diagonal
+  int b_upper;          // B is upper triangular: k-loop stops at the tile's last column
 };
 
 namespace zg {
@@ -90,7 +92,11 @@ __global__ void __launch_bounds__(zg::Cfg<BM, BN>::THREADS, 1)
   const int in_group = blockIdx.x % per_group;
   const int m0 = (first_m + in_group % gsize) * BM;
   const int n0 = (in_group / gsize) * BN;
-  const int KT = (p.K + BK - 1) / BK;
+  // structure flags: upper_only skips tiles strictly below the diagonal (Hermitian results whose
+  // lower triangle is never read, e.g. Gram matrices for Cholesky); b_upper truncates the k-loop
+  // at the tile's last column when B is upper triangular (V R^{-1}).
+  if (p.upper_only && m0 >= n0 + BN) return;
+  const int KT = p.b_upper ? (min(p.K, n0 + BN) + BK - 1) / BK : (p.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {

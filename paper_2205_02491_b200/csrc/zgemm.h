@@ -15,6 +15,8 @@ struct ZgemmDesc {
   const void* S = nullptr; int64_t lds = 0;   // shift source (may be null)
   int shift_lo = 0, shift_hi = 0; int64_t shift_off = 0;
   bool use3m = false;            // 3M (Gauss) complex product: 3 real DMMAs per complex MAC
+  bool upper_only = false;       // only tiles on/above the diagonal are computed (Hermitian C)
+  bool b_upper = false;          // B upper triangular (zeros below the diagonal are skipped)
 };
 
 // C = alpha*op(A)*B - alpha*gamma*S[shift rows] + beta*C   (all complex double, column-major)

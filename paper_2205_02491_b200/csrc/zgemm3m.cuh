@@ -53,7 +53,11 @@ __global__ void __launch_bounds__(CFG::THREADS, 1)
   const int in_group = blockIdx.x % per_group;
   const int m0 = (first_m + in_group % gsize) * BM;
   const int n0 = (in_group / gsize) * BN;
-  const int KT = (p.K + BK - 1) / BK;
+  // structure flags: upper_only skips tiles strictly below the diagonal (Hermitian results whose
+  // lower triangle is never read, e.g. Gram matrices for Cholesky); b_upper truncates the k-loop
+  // at the tile's last column when B is upper triangular (V R^{-1}).
+  if (p.upper_only && m0 >= n0 + BN) return;
+  const int KT = p.b_upper ? (min(p.K, n0 + BN) + BK - 1) / BK : (p.K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
