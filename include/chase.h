@@ -64,7 +64,9 @@ typedef struct {
   int32_t rank, world_size;       /* rank = i + j*r */
   const void* nccl_unique_id;     /* 128-byte ncclUniqueId, identical on all ranks; NULL if world_size == 1 */
   int32_t cuda_device;
-  void* cuda_stream;              /* cudaStream_t to order against (e.g. torch's current stream); may be NULL */
+  void* cuda_stream;              /* cudaStream_t the caller produces inputs on (e.g. torch's current
+                                     stream); every call waits for work already queued on it.
+                                     NULL = the legacy default stream. */
 } chase_init_args;
 
 typedef struct {

@@ -116,6 +116,11 @@ class Chase:
             self._id = C.create_string_buffer(bytes(nccl_id), 128)
             args.nccl_unique_id = C.cast(self._id, C.c_void_p)
         args.cuda_device = int(device)
+        if stream is None:
+            # order every library call after the caller's current torch stream (inputs written by
+            # torch kernels must be complete before the library's own stream reads them)
+            import torch
+            stream = torch.cuda.current_stream(int(device)).cuda_stream
         args.cuda_stream = C.c_void_p(stream) if stream else None
         st = self.lib.chase_init(C.byref(self._h), C.byref(args))
         if st != CHASE_OK:

@@ -297,7 +297,9 @@ chase_status chase_init(chase_handle** out, const chase_init_args* a) {
     if (major < 10) throw UsageError("this library requires an sm_100a (B200) device");
     h->grid.setup(a->N, r, c, a->rank);
     CHASE_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    h->user_stream = reinterpret_cast<cudaStream_t>(a->cuda_stream);
+    // NULL means the caller's work is on the legacy default stream; the library stream is
+    // non-blocking, so ordering against it must be explicit (an event on cudaStreamLegacy).
+    h->user_stream = a->cuda_stream ? reinterpret_cast<cudaStream_t>(a->cuda_stream) : cudaStreamLegacy;
     CHASE_CUDA(cudaEventCreate(&h->ev0));
     CHASE_CUDA(cudaEventCreate(&h->ev1));
     if (ws > 1) {
