@@ -115,10 +115,85 @@ class G2Matrix:
         return self.phi[:, None] * X
 
 
-class G1Matrix:
-    """Paper's construction A = Q^T D Q, complexified: Haar Q, n <= 4096."""
+class R2Matrix:
+    """Real-symmetric analogue of G2 for the real variant (the paper's matrices are real,
+    P:134):  H = S P C P^T S with C = Hc diag(lambda_pi) Hc, Hc the orthogonal, symmetric
+    discrete Hartley matrix Hc_{jk} = cas(2 pi j k / n)/sqrt(n) (cas = cos + sin).  Since
+    cas(a) cas(b) = cos(a - b) + sin(a + b),
+        C_{jl} = u[(j - l) mod n] + w[(j + l) mod n],   u + i w = ifft(lambda_pi),
+    P = four real Householder reflectors (rank-2 updates as in G2), S = diag(+-1) random signs.
+    Exact spectrum; eigenvector of lambda_pi[k] = S P h_k (h_k = column k of Hc)."""
 
-    def __init__(self, lam: np.ndarray, seed: int = 1):
+    def __init__(self, lam: np.ndarray, seed: int = 1, n_reflectors: int = 4):
+        lam = np.asarray(lam, dtype=np.float64)
+        n = lam.shape[0]
+        self.n = n
+        self.lam = np.sort(lam)
+        rng = np.random.default_rng(seed)
+        self.perm = rng.permutation(n)
+        lam_p = self.lam[self.perm]
+        self.lam_p = lam_p
+        c = np.fft.ifft(lam_p)
+        self.u, self.w = np.ascontiguousarray(c.real), np.ascontiguousarray(c.imag)
+        self.sgn = np.where(rng.uniform(size=n) < 0.5, -1.0, 1.0)
+        ys = []
+        for _ in range(n_reflectors):
+            y = rng.standard_normal(n)
+            ys.append(y / np.linalg.norm(y))
+        self.ys = ys
+        U = np.zeros((n, 0))
+        V = np.zeros((n, 0))
+
+        def dht(x):                     # Hc x
+            f = np.fft.fft(x)
+            return (f.real - f.imag) / np.sqrt(n)
+
+        for y in reversed(ys):
+            z = dht(lam_p * dht(y)) + U @ (V.T @ y)                 # z = M y
+            s = float(y @ z)
+            w = -2.0 * z + 2.0 * s * y
+            U = np.concatenate([U, y[:, None], w[:, None]], axis=1)
+            V = np.concatenate([V, w[:, None], y[:, None]], axis=1)
+        self.U = self.sgn[:, None] * U
+        self.V = self.sgn[:, None] * V
+        self.rank = U.shape[1]
+
+    def block(self, r0, nr, c0, nc):
+        rows = np.arange(r0, r0 + nr)
+        cols = np.arange(c0, c0 + nc)
+        dm = (rows[:, None] - cols[None, :]) % self.n
+        dp = (rows[:, None] + cols[None, :]) % self.n
+        h = self.sgn[rows][:, None] * self.sgn[cols][None, :]
+        h = h * (self.u[dm] + self.w[dp])
+        for t in range(self.rank):
+            h = h + self.U[rows, t][:, None] * self.V[cols, t][None, :]
+        return h
+
+    def dense(self):
+        return self.block(0, self.n, 0, self.n)
+
+    def params_for_device(self):
+        return dict(n=self.n, rank=self.rank, u=self.u.copy(), w=self.w.copy(), sgn=self.sgn.copy(),
+                    U=np.ascontiguousarray(self.U.ravel()), V=np.ascontiguousarray(self.V.ravel()))
+
+    def eigvecs(self, idx):
+        idx = np.atleast_1d(np.asarray(idx))
+        inv = np.empty(self.n, dtype=np.int64)
+        inv[self.perm] = np.arange(self.n)
+        ks = inv[idx]
+        j = np.arange(self.n)
+        ang = 2 * np.pi * np.outer(j, ks) / self.n
+        X = (np.cos(ang) + np.sin(ang)) / np.sqrt(self.n)
+        for y in reversed(self.ys):
+            X = X - 2.0 * np.outer(y, y @ X)
+        return self.sgn[:, None] * X
+
+
+class G1Matrix:
+    """Paper's construction A = Q^T D Q: Haar Q (complex by default -- ledger #11 --
+    real orthogonal with real=True, the paper's own setting), n <= 4096."""
+
+    def __init__(self, lam: np.ndarray, seed: int = 1, real: bool = False):
         lam = np.sort(np.asarray(lam, dtype=np.float64))
         n = lam.shape[0]
         if n > 4096:
@@ -126,7 +201,10 @@ class G1Matrix:
         self.n = n
         self.lam = lam
         rng = np.random.default_rng(seed)
-        Z = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2.0)
+        if real:
+            Z = rng.standard_normal((n, n))
+        else:
+            Z = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(2.0)
         Q, R = np.linalg.qr(Z)
         dr = np.diag(R)
         Q = Q * (dr / np.abs(dr))[None, :]
@@ -146,12 +224,17 @@ class G1Matrix:
 
 def make_matrix(family: str, n: int, kind: str = "g2", seed: int = 1,
                 d_max: float = 1.0, eps: float = 1e-4):
-    """Seeded test matrix of Table 1 `family` with exact spectrum `.lam`."""
+    """Seeded test matrix of Table 1 `family` with exact spectrum `.lam`.
+    kind: g1 / g2 (complex Hermitian), r1 / r2 (real symmetric: real Haar Q / Hartley-based)."""
     lam = _spectrum(family, n, d_max, eps)
     if kind == "g1":
         return G1Matrix(lam, seed)
     if kind == "g2":
         return G2Matrix(lam, seed)
+    if kind == "r1":
+        return G1Matrix(lam, seed, real=True)
+    if kind == "r2":
+        return R2Matrix(lam, seed)
     raise ValueError(kind)
 
 

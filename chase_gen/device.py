@@ -23,6 +23,8 @@ def _load():
                                             C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.chase_gen_g2_block.restype = C.c_int
+        _lib.chase_gen_r2_block.argtypes = _lib.chase_gen_g2_block.argtypes + [C.c_void_p]
+        _lib.chase_gen_r2_block.restype = C.c_int
     return _lib
 
 
@@ -51,3 +53,34 @@ class DeviceG2:
         if rc != 0:
             raise RuntimeError(f"chase_gen_g2_block failed: cuda error {rc}")
         return out
+
+
+class DeviceR2:
+    """Device description of an R2Matrix (real symmetric); `fill` writes a float64 block."""
+
+    def __init__(self, r2, device="cuda"):
+        import torch
+        prm = r2.params_for_device()
+        self.n, self.rank = prm["n"], prm["rank"]
+        t = lambda a: torch.from_numpy(a).to(device)
+        self.u, self.w, self.sgn, self.U, self.V = t(prm["u"]), t(prm["w"]), t(prm["sgn"]), t(prm["U"]), t(prm["V"])
+
+    def fill(self, out, r0, c0):
+        import torch
+        nr, nc = out.shape
+        ld = out.stride(1) if nc > 1 else nr
+        assert (out.stride(0) == 1 or nr == 1) and out.dtype == torch.float64
+        st = torch.cuda.current_stream(out.device).cuda_stream
+        rc = _load().chase_gen_r2_block(C.c_void_p(out.data_ptr()), ld, r0, nr, c0, nc, self.n, self.rank,
+                                        C.c_void_p(self.u.data_ptr()), C.c_void_p(self.w.data_ptr()),
+                                        C.c_void_p(self.sgn.data_ptr()), C.c_void_p(self.U.data_ptr()),
+                                        C.c_void_p(self.V.data_ptr()), C.c_void_p(st))
+        if rc != 0:
+            raise RuntimeError(f"chase_gen_r2_block failed: cuda error {rc}")
+        return out
+
+
+def device_matrix(M, device="cuda"):
+    """Device twin for a G2Matrix (complex) or R2Matrix (real)."""
+    from .dense import R2Matrix
+    return DeviceR2(M, device) if isinstance(M, R2Matrix) else DeviceG2(M, device)

@@ -51,10 +51,15 @@ typedef enum {
   CHASE_E_MAXITER = 8   /* max_iter reached; `locked` pairs in the report are valid */
 } chase_status;
 
-typedef enum { CHASE_C128 = 0 /* complex<double>, interleaved */, CHASE_C64 = 1 /* reserved */ } chase_dtype;
+typedef enum {
+  CHASE_C128 = 0, /* complex<double>, interleaved (re, im): Hermitian H -- the north_star path */
+  CHASE_C64 = 1,  /* reserved (complex single) */
+  CHASE_R64 = 2   /* double: real symmetric H, the paper's own experimental field.
+                     Every buffer argument is then real double with the same layouts. */
+} chase_dtype;
 
 typedef struct {
-  chase_dtype dtype;              /* only CHASE_C128 is implemented */
+  chase_dtype dtype;              /* CHASE_C128 or CHASE_R64 */
   int64_t N;                      /* matrix order */
   int32_t nev_max, nex_max;       /* workspace sizing */
   int32_t grid_rows, grid_cols;   /* r, c; 0,0 = 1 x world.  world_size == 1 with r*c > 1 selects

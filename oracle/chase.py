@@ -76,7 +76,7 @@ def chebyshev_filter(H, V, degrees, b_sup, mu_1, mu_ne):
     degree is exhausted (P:329 'Sort ... according to m').  Serial 1x1 semantics.
     Returns (filtered V, matvecs = sum_a m_a  (P:729-731 footnote))."""
     degrees = np.asarray(degrees, dtype=np.int64)
-    V = np.array(V, dtype=np.complex128, copy=True)
+    V = np.array(V, dtype=np.result_type(H, V, np.float64), copy=True)
     kmax = int(degrees.max()) if degrees.size else 0
     if kmax == 0:
         return V, 0
@@ -136,6 +136,8 @@ def lanczos(H, n_e: int, steps: int = 25, runs: int = 4, seed: int = 3, start=No
     N = H.shape[0]
     if start is None:
         start = random_block(seed, 0, N, 0, runs, STREAM_LANCZOS)
+        if not np.iscomplexobj(H):
+            start = start.real          # real-symmetric variant: real part of the same draw
     steps = min(steps, N)
     thetas, weights = [], []
     b_sup = -np.inf
@@ -185,7 +187,7 @@ def qr_locked(Y, V):
     as is; the active block is made orthogonal to Y (two classical Gram-Schmidt passes) and then
     factored by Householder QR (deliberately a different algorithm from the GPU's CholQR2).
     The Q factor is normalised so that R has a positive real diagonal (the unique thin QR)."""
-    V = np.array(V, dtype=np.complex128, copy=True)
+    V = np.array(V, copy=True)
     if Y is not None and Y.shape[1] > 0:
         for _ in range(2):
             V = V - Y @ (Y.conj().T @ V)
@@ -267,8 +269,11 @@ def chase_solve(H, nev: int, nex: int, deg: int = 20, tol: float = 1e-10, deg_ma
                 seed_v: int = 2, seed_lanczos: int = 3, largest: bool = False, V0=None,
                 lanczos_res: LanczosResult | None = None):
     """Alg. 1, serial semantics.  Returns (eigenvalues[nev] ascending,
-    eigenvectors N x nev, Report).  `largest` solves on -H (ledger #17)."""
-    H = np.asarray(H, dtype=np.complex128)
+    eigenvectors N x nev, Report).  `largest` solves on -H (ledger #17).  A real H selects the
+    real-symmetric variant (the paper's setting): float64 arithmetic, real start vectors
+    (the real part of the same counter-based draw)."""
+    real = not np.iscomplexobj(H)
+    H = np.asarray(H, dtype=np.float64 if real else np.complex128)
     if largest:
         H = -H
     N = H.shape[0]
@@ -279,7 +284,11 @@ def chase_solve(H, nev: int, nex: int, deg: int = 20, tol: float = 1e-10, deg_ma
     lz = lanczos_res or lanczos(H, n_e, lanczos_steps, lanczos_runs, seed_lanczos)   # line 2
     b_sup, mu_1, mu_ne, nu = lz.b_sup, lz.mu_1, lz.mu_ne, lz.nu
     rep.b_sup, rep.nu = b_sup, nu
-    V = random_block(seed_v, 0, N, 0, n_e, STREAM_START_V) if V0 is None else np.array(V0, dtype=np.complex128)
+    if V0 is None:
+        V = random_block(seed_v, 0, N, 0, n_e, STREAM_START_V)
+        V = V.real.copy() if real else V
+    else:
+        V = np.array(V0, dtype=H.dtype)
     ritz = np.zeros(n_e)
     res = np.zeros(n_e)
     m = np.full(n_e, deg + (deg % 2), dtype=np.int64)                  # line 1 (even)

@@ -101,13 +101,16 @@ def _ld(t):
 class Chase:
     """One rank's handle.  All collective methods must be called by every rank of the grid."""
 
+    C128, R64 = 0, 2          # chase_dtype: complex Hermitian / real symmetric (f2)
+
     def __init__(self, N, nev_max, nex_max, grid=(1, 1), rank=0, world_size=1, nccl_id=None,
-                 device=0, stream=None):
+                 device=0, stream=None, dtype="c128"):
         self.lib = load()
         self._h = C.c_void_p()
         self._id = None
         args = InitArgs()
-        args.dtype = 0
+        self.real = dtype in ("r64", "float64", 2)
+        args.dtype = self.R64 if self.real else self.C128
         args.N = int(N)
         args.nev_max, args.nex_max = int(nev_max), int(nex_max)
         args.grid_rows, args.grid_cols = int(grid[0]), int(grid[1])
@@ -194,7 +197,8 @@ class Chase:
         r0, p, c0, q = self.local_layout()
         vals = (C.c_double * nev)()
         if vectors is None:
-            vectors = torch.empty((nev + nex, q), dtype=torch.complex128, device=H.device).t()
+            vectors = torch.empty((nev + nex, q), dtype=torch.float64 if self.real else torch.complex128,
+                                  device=H.device).t()
         elif vectors.shape[0] != q:
             raise ValueError("vectors must be V-layout (q rows)")
         rep = Report()

@@ -18,14 +18,15 @@ unsigned long long g_kernel_launches = 0;
 void allreduce_block(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows,
                      int64_t ld, int ncols) {
   if (comm_size <= 1 || !comm || ncols <= 0 || rows <= 0) return;   // !comm: emulated grid
+  const int nd = h->nd();
   if (ld == rows) {
-    CHASE_NCCL(ncclAllReduce(Y, Y, (size_t)(2 * rows * ncols), ncclDouble, ncclSum, comm, h->stream));
+    CHASE_NCCL(ncclAllReduce(Y, Y, (size_t)(nd * rows * ncols), ncclDouble, ncclSum, comm, h->stream));
     return;
   }
   CHASE_NCCL(ncclGroupStart());
   for (int c = 0; c < ncols; ++c) {
-    double2* col = reinterpret_cast<double2*>(Y) + (int64_t)c * ld;
-    CHASE_NCCL(ncclAllReduce(col, col, (size_t)(2 * rows), ncclDouble, ncclSum, comm, h->stream));
+    double* col = reinterpret_cast<double*>(Y) + (int64_t)c * ld * nd;
+    CHASE_NCCL(ncclAllReduce(col, col, (size_t)(nd * rows), ncclDouble, ncclSum, comm, h->stream));
   }
   CHASE_NCCL(ncclGroupEnd());
 }
@@ -33,6 +34,12 @@ void allreduce_block(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, i
 void allreduce_doubles(chase_handle* h, ncclComm_t comm, int comm_size, double* x, size_t n) {
   if (comm_size <= 1 || !comm || n == 0) return;
   CHASE_NCCL(ncclAllReduce(x, x, n, ncclDouble, ncclSum, comm, h->stream));
+}
+
+// complex (3M / 4M) or real GEMM by the handle's dtype
+void gemm(chase_handle* h, const ZgemmDesc& d) {
+  if (h->real()) dgemm(d, h->stream);
+  else zgemm(d, h->stream);
 }
 
 // ------------------------------------------------------------------- fused recurrence step
@@ -73,7 +80,7 @@ void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void*
                void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma) {
   if (ncols <= 0) return;
   const Grid& g = h->grid;
-  zgemm(step_desc(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma), h->stream);
+  gemm(h, step_desc(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma));
   if (dir == 0)
     allreduce_block(h, h->rowc, g.c, Y, g.rows.len, ldy, ncols);     // row communicator
   else
@@ -101,8 +108,9 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
   if (!(e > 0.0)) throw UsageError("filter interval is empty (b_sup <= mu_ne)");
   const double sigma1 = e / (mu_1 - c);
   double sigma_prev = sigma1;
-  double2* Vz = reinterpret_cast<double2*>(V);
-  double2* Wz = reinterpret_cast<double2*>(W);
+  char* Vz = reinterpret_cast<char*>(V);
+  char* Wz = reinterpret_cast<char*>(W);
+  const int64_t es = (int64_t)h->es();
   const Grid& g = h->grid;
   // Overlap: on a real grid the columns are cut into chunks with fixed absolute
   // boundaries; each chunk's all-reduce runs on the comm stream while the next chunk's GEMM runs,
@@ -137,12 +145,12 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       sigma_prev = sigma;
     }
     const int dir = (k & 1) ? 0 : 1;        // odd: forward V -> W; even: backward W -> V
-    double2* X = dir == 0 ? Vz : Wz;
-    double2* Y = dir == 0 ? Wz : Vz;
+    char* X = dir == 0 ? Vz : Wz;
+    char* Y = dir == 0 ? Wz : Vz;
     const int64_t ldx = dir == 0 ? ldv : ldw, ldy = dir == 0 ? ldw : ldv;
     if (!comm) {
-      hemm_step(h, dir, H, ldh, X + (int64_t)first * ldx, ldx, Y + (int64_t)first * ldy, ldy, ncols - first,
-                alpha, beta, c);
+      hemm_step(h, dir, H, ldh, X + (int64_t)first * ldx * es, ldx, Y + (int64_t)first * ldy * es, ldy,
+                ncols - first, alpha, beta, c);
       continue;
     }
     const int64_t rows = dir == 0 ? g.rows.len : g.cols.len;
@@ -150,16 +158,16 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       const int lo = std::max(first, bnd[ch]), hi = bnd[ch + 1];
       if (lo >= hi) continue;
       if (rec[(k - 1) & 1][ch]) CHASE_CUDA(cudaStreamWaitEvent(h->stream, h->ev_comm[(k - 1) & 1][ch], 0));
-      zgemm(step_desc(h, dir, H, ldh, X + (int64_t)lo * ldx, ldx, Y + (int64_t)lo * ldy, ldy, hi - lo, alpha,
-                      beta, c), h->stream);
+      gemm(h, step_desc(h, dir, H, ldh, X + (int64_t)lo * ldx * es, ldx, Y + (int64_t)lo * ldy * es, ldy, hi - lo,
+                        alpha, beta, c));
       CHASE_CUDA(cudaEventRecord(h->ev_gemm[ch], h->stream));
       CHASE_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_gemm[ch], 0));
       cudaStream_t saved = h->stream;
       h->stream = h->comm_stream;               // allreduce_block enqueues on h->stream
       if (dir == 0)
-        allreduce_block(h, h->rowc, g.c, Y + (int64_t)lo * ldy, rows, ldy, hi - lo);
+        allreduce_block(h, h->rowc, g.c, Y + (int64_t)lo * ldy * es, rows, ldy, hi - lo);
       else
-        allreduce_block(h, h->colc, g.r, Y + (int64_t)lo * ldy, rows, ldy, hi - lo);
+        allreduce_block(h, h->colc, g.r, Y + (int64_t)lo * ldy * es, rows, ldy, hi - lo);
       h->stream = saved;
       CHASE_CUDA(cudaEventRecord(h->ev_comm[k & 1][ch], h->comm_stream));
       rec[k & 1][ch] = true;
@@ -188,14 +196,33 @@ __global__ void k_random_block(double2* V, int64_t ldv, int64_t rows, int64_t gr
   }
 }
 
+// real variant: the real part of the same counter-based entry
+__global__ void k_random_block_real(double* V, int64_t ldv, int64_t rows, int64_t grow0, int col0, int ncols,
+                                    uint32_t k0, uint32_t k1, uint32_t stream_id) {
+  const int64_t total = rows * ncols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rloc = idx % rows;
+    const int cl = (int)(idx / rows);
+    const uint64_t grow = (uint64_t)(grow0 + rloc);
+    const Philox4 o = philox4x32_10((uint32_t)grow, (uint32_t)(grow >> 32), (uint32_t)(col0 + cl),
+                                    stream_id, k0, k1);
+    V[rloc + (int64_t)cl * ldv] = philox_unit(o.x[0], o.x[1]);
+  }
+}
+
 void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
                   int ncols, uint64_t seed, uint32_t stream_id) {
   if (rows <= 0 || ncols <= 0) return;
   const int64_t total = rows * ncols;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  k_random_block<<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double2*>(V), ldv, rows, grow0,
-                                                col0, ncols, (uint32_t)seed, (uint32_t)(seed >> 32),
-                                                stream_id);
+  if (h->real())
+    k_random_block_real<<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double*>(V), ldv, rows, grow0, col0, ncols,
+                                                       (uint32_t)seed, (uint32_t)(seed >> 32), stream_id);
+  else
+    k_random_block<<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double2*>(V), ldv, rows, grow0,
+                                                  col0, ncols, (uint32_t)seed, (uint32_t)(seed >> 32),
+                                                  stream_id);
   CHASE_CHECK_LAUNCH();
 }
 
@@ -278,7 +305,8 @@ chase_status chase_init(chase_handle** out, const chase_init_args* a) {
   *out = nullptr;
   chase_handle* h = new chase_handle();
   try {
-    if (a->dtype != CHASE_C128) throw UsageError("only CHASE_C128 is implemented");
+    if (a->dtype != CHASE_C128 && a->dtype != CHASE_R64) throw UsageError("dtype must be CHASE_C128 or CHASE_R64");
+    h->dtype = a->dtype;
     if (a->N <= 0 || a->nev_max <= 0 || a->nex_max <= 0 || a->nev_max + (int64_t)a->nex_max > a->N)
       throw UsageError("invalid N / nev_max / nex_max");
     int ws = std::max(1, a->world_size);

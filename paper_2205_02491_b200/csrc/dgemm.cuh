@@ -1,0 +1,193 @@
+// Real-double GEMM with the fused Chebyshev-step epilogue: the real-symmetric variant (
+// the paper's own experiments are real symmetric).
+//
+//   C[M x N] = alpha * op(A) * B  -  alpha*gamma * S[shift rows]  +  beta * C,  op(A) = A or A^T
+//
+// FP64 DMMA.8x8x4 (one MMA per real multiply-add).  8 warps of 64 (m) x 32 (n) accumulators
+// (128 registers) on a 128 x 128 CTA tile, BK = 32 real k per stage, 3-stage ring.  Operand tiles
+// are staged with cp.async (8-byte, zero-filled out of bounds): real shards may have odd leading
+// dimensions and odd row offsets, which TMA's 16-byte alignment rules exclude.  Shared memory uses
+// the same XOR-128B swizzle as the TMA path: 128-byte rows of 16 doubles, 16-byte chunk index XOR
+// (row % 8).  With the k permutation kk(t, s) = 2 s + (t & 1) + 8 (t >> 1) the 16 lanes of a
+// half-warp read 8 distinct chunks x 2 halves (conflict-free) for B and transposed A; forward-A
+// rows hold 16 m values and are read 2-way conflicted (8 of 12 fragment loads per 32 DMMAs).
+#pragma once
+#include "common.cuh"
+#include "tma.cuh"
+#include "zgemm.cuh"
+
+namespace chase {
+
+struct DCfg {
+  static constexpr int WM = 2, WN = 4, STAGES = 3;
+  static constexpr int BM = 64 * WM, BN = 32 * WN, BK = 32;
+  static constexpr int NWARPS = WM * WN, THREADS = NWARPS * 32;
+  static constexpr uint32_t A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8, STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+};
+
+struct DgemmParams {
+  int M, N, K;
+  double alpha, beta, gamma;
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  const double* S;
+  int64_t lds;
+  int shift_lo, shift_hi;
+  int64_t shift_off;
+  double* C;
+  int64_t ldc;
+  int upper_only;
+  int b_upper;
+};
+
+namespace dg {
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool pred) {
+  const int sz = pred ? 8 : 0;   // src-size 0 -> zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+// byte offset of element (row r of 128 B, index x in [0,16)) in a swizzled tile
+__device__ __forceinline__ uint32_t soff(int r, int x) {
+  return (uint32_t)(r * 128 + ((((x >> 1) ^ (r & 7))) << 4) + ((x & 1) << 3));
+}
+}  // namespace dg
+
+template <bool TRANS_A>
+__global__ void __launch_bounds__(DCfg::THREADS, 1) dgemm_dmma_kernel(DgemmParams p) {
+  constexpr int WN = DCfg::WN, STAGES = DCfg::STAGES, BM = DCfg::BM, BN = DCfg::BN, BK = DCfg::BK;
+  constexpr int THREADS = DCfg::THREADS;
+  constexpr uint32_t A_BYTES = DCfg::A_BYTES, STAGE_BYTES = DCfg::STAGE_BYTES;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int tiles_m = (p.M + BM - 1) / BM;
+  constexpr int GROUP_M = 8;
+  const int per_group = GROUP_M * tiles_n;
+  const int group = blockIdx.x / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(tiles_m - first_m, GROUP_M);
+  const int in_group = blockIdx.x % per_group;
+  const int m0 = (first_m + in_group % gsize) * BM;
+  const int n0 = (in_group / gsize) * BN;
+  if (p.upper_only && m0 >= n0 + BN) return;
+  const int KT = p.b_upper ? (min(p.K, n0 + BN) + BK - 1) / BK : (p.K + BK - 1) / BK;
+  const uint32_t smem_base = smem_u32(smem);
+
+  // cooperative staging of k-tile kt into slot kt % STAGES
+  auto stage_load = [&](int kt) {
+    const uint32_t sa = smem_base + (kt % STAGES) * STAGE_BYTES;
+    const uint32_t sb = sa + A_BYTES;
+    const int k0 = kt * BK;
+    // A: BM x BK elements
+#pragma unroll 2
+    for (int it = 0; it < (BM * BK) / THREADS; ++it) {
+      const int e = tid + it * THREADS;
+      if constexpr (!TRANS_A) {
+        // A col-major M x K (m contiguous): smem [BM/16][BK][16 m]
+        const int m = e % BM, k = e / BM;
+        const int gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        const double* src = p.A + (ok ? (int64_t)gm + (int64_t)gk * p.lda : 0);
+        dg::cp_async8(sa + dg::soff((m >> 4) * BK + k, m & 15), src, ok);
+      } else {
+        // A col-major K x M (k contiguous), op = A^T: smem [BK/16][BM][16 k]
+        const int k = e % BK, m = e / BK;
+        const int gm = m0 + m, gk = k0 + k;
+        const bool ok = gm < p.M && gk < p.K;
+        const double* src = p.A + (ok ? (int64_t)gk + (int64_t)gm * p.lda : 0);
+        dg::cp_async8(sa + dg::soff((k >> 4) * BM + m, k & 15), src, ok);
+      }
+    }
+    // B: BK x BN, col-major (k contiguous): smem [BK/16][BN][16 k]
+#pragma unroll 2
+    for (int it = 0; it < (BK * BN) / THREADS; ++it) {
+      const int e = tid + it * THREADS;
+      const int k = e % BK, n = e / BK;
+      const int gk = k0 + k, gn = n0 + n;
+      const bool ok = gk < p.K && gn < p.N;
+      const double* src = p.B + (ok ? (int64_t)gk + (int64_t)gn * p.ldb : 0);
+      dg::cp_async8(sb + dg::soff((k >> 4) * BN + n, k & 15), src, ok);
+    }
+  };
+
+#pragma unroll
+  for (int kt = 0; kt < STAGES - 1; ++kt) {
+    if (kt < KT) stage_load(kt);
+    dg::cp_commit();
+  }
+
+  const int wm = warp / WN, wn = warp % WN;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    dg::cp_wait<STAGES - 2>();
+    __syncthreads();                         // tile kt visible; slot of tile kt-1 free
+    if (kt + STAGES - 1 < KT) stage_load(kt + STAGES - 1);
+    dg::cp_commit();
+    const uint32_t sa = smem_base + (kt % STAGES) * STAGE_BYTES;
+    const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int kc = ks >> 2;
+      const int kk = 2 * (ks & 3) + (t & 1) + 8 * (t >> 1);
+      double a[8], b[4];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        if constexpr (!TRANS_A) {
+          const int m = wm * 64 + mt * 8 + g;
+          a[mt] = dg::lds64(sa + dg::soff((m >> 4) * BK + kc * 16 + kk, m & 15));
+        } else {
+          a[mt] = dg::lds64(sa + dg::soff(kc * BM + wm * 64 + mt * 8 + g, kk));
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) b[nt] = dg::lds64(sb + dg::soff(kc * BN + wn * 32 + nt * 8 + g, kk));
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) zg::dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+    }
+  }
+  dg::cp_wait<0>();
+
+  const double ag = p.alpha * p.gamma;
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    const int m = m0 + wm * 64 + mt * 8 + g;
+    if (m >= p.M) continue;
+    const bool shifted = (m >= p.shift_lo) && (m < p.shift_hi);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = n0 + wn * 32 + nt * 8 + 2 * t + j;
+        if (n >= p.N) continue;
+        double v = p.alpha * acc[mt][nt][j];
+        if (shifted) v -= ag * p.S[(int64_t)m + p.shift_off + (int64_t)n * p.lds];
+        double* cp = p.C + (int64_t)m + (int64_t)n * p.ldc;
+        if (p.beta != 0.0) v += p.beta * *cp;
+        *cp = v;
+      }
+    }
+  }
+}
+
+}  // namespace chase

@@ -65,6 +65,10 @@ struct Options {
 
 struct chase_handle {
   chase::Grid grid;
+  int dtype = CHASE_C128;              // CHASE_C128 (complex Hermitian) or CHASE_R64 (real symmetric)
+  bool real() const { return dtype == CHASE_R64; }
+  size_t es() const { return real() ? 8 : 16; }          // bytes per element
+  int nd() const { return real() ? 1 : 2; }              // doubles per element
   int device = 0;
   int world_size = 1;
   cudaStream_t stream = nullptr;       // library stream (all kernels, NCCL)
@@ -86,6 +90,8 @@ struct chase_handle {
 
 namespace chase {
 
+// complex (3M / 4M) or real GEMM by the handle's dtype, on the handle's stream
+void gemm(chase_handle* h, const ZgemmDesc& d);
 // one fused distributed recurrence step (a2/a3 or a4/a5); see chase.h chase_hemm_step
 void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
                void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma);

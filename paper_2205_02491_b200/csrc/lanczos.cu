@@ -14,24 +14,26 @@
 #include <vector>
 #include "dense.h"
 #include "handle.h"
+#include "scalar.cuh"
 
 namespace chase {
 
 namespace {
-// h[k*L + r] = Q_k[:, r]^H F[:, r] for k <= j (complex, 2 doubles each); pass 1 of 2
-__global__ void k_proj_p1(const double2* Q, int64_t N, int L, int nk, const double2* F, int chunks, double* part) {
+// h[k*L + r] = Q_k[:, r]^H F[:, r] for k <= j (2 doubles each: re, im); pass 1 of 2
+template <class T>
+__global__ void k_proj_p1(const T* Q, int64_t N, int L, int nk, const T* F, int chunks, double* part) {
   __shared__ double sh[2][256];
   const int col = blockIdx.x;          // col = k*L + r
   const int r = col % L, chunk = blockIdx.y;
   const int64_t len = (N + chunks - 1) / chunks;
   const int64_t i0 = chunk * len, i1 = min(N, i0 + len);
-  const double2* q = Q + (int64_t)col * N;
-  const double2* f = F + (int64_t)r * N;
+  const T* q = Q + (int64_t)col * N;
+  const T* f = F + (int64_t)r * N;
   double re = 0.0, im = 0.0;
   for (int64_t i = i0 + threadIdx.x; i < i1; i += 256) {
-    const double2 a = q[i], b = f[i];
-    re += a.x * b.x + a.y * b.y;
-    im += a.x * b.y - a.y * b.x;
+    const T d = SC<T>::mulc(q[i], f[i]);
+    re += SC<T>::re(d);
+    im += SC<T>::im(d);
   }
   sh[0][threadIdx.x] = re;
   sh[1][threadIdx.x] = im;
@@ -56,31 +58,30 @@ __global__ void k_proj_p2(const double* part, int chunks, int ncols, double* h) 
 }
 
 // F[:, r] -= sum_k Q_k[:, r] h[k*L + r]
-__global__ void k_proj_sub(const double2* Q, int64_t N, int L, int nk, const double* h, double2* F) {
+template <class T>
+__global__ void k_proj_sub(const T* Q, int64_t N, int L, int nk, const double* h, T* F) {
   const int64_t total = N * L;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % N;
     const int r = (int)(idx / N);
-    double2 f = F[i + (int64_t)r * N];
+    T f = F[i + (int64_t)r * N];
     for (int k = 0; k < nk; ++k) {
-      const double2 q = Q[i + (int64_t)(k * L + r) * N];
-      const double hr = h[2 * (k * L + r)], hi = h[2 * (k * L + r) + 1];
-      f.x -= q.x * hr - q.y * hi;
-      f.y -= q.x * hi + q.y * hr;
+      const T q = Q[i + (int64_t)(k * L + r) * N];
+      f = SC<T>::sub(f, SC<T>::mul(q, SC<T>::make(h[2 * (k * L + r)], h[2 * (k * L + r) + 1])));
     }
     F[i + (int64_t)r * N] = f;
   }
 }
 
-// Q_next[:, r] = F[:, r] / beta_r  (0 if beta_r is 0); beta2 = squared norms (real parts of dots)
-__global__ void k_normalize(const double2* F, int64_t N, int L, const double* dots, double2* Qn) {
+// Q_next[:, r] = F[:, r] / beta_r  (0 if beta_r is 0); dots = squared norms (real parts)
+template <class T>
+__global__ void k_normalize(const T* F, int64_t N, int L, const double* dots, T* Qn) {
   const int64_t total = N * L;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(idx / N);
     const double b2 = dots[2 * r];
-    const double s = b2 > 0.0 ? 1.0 / sqrt(b2) : 0.0;
-    const double2 f = F[idx];
-    Qn[idx] = make_double2(f.x * s, f.y * s);
+    const double sc = b2 > 0.0 ? 1.0 / sqrt(b2) : 0.0;
+    Qn[idx] = SC<T>::scale(F[idx], sc);
   }
 }
 
@@ -121,7 +122,8 @@ void host_syev(int m, std::vector<double>& A, std::vector<double>& Z) {
 }
 }  // namespace
 
-LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
+template <class T>
+static LanczosOut lanczos_t(chase_handle* h, const void* H, int64_t ldh, int n_e) {
   const Grid& g = h->grid;
   const int64_t N = g.N;
   const int L = h->opt.lanczos_runs;
@@ -130,22 +132,22 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
   const double hsign = h->opt.largest ? -1.0 : 1.0;
   // buffers: Q (N x L x (m+1)), F (N x L), part, h coefficients, per-step dots
   const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(32, (N + 8191) / 8192));
-  const size_t qbytes = 16 * (size_t)N * L * (m + 1), fbytes = 16 * (size_t)N * L;
+  const size_t qbytes = sizeof(T) * (size_t)N * L * (m + 1), fbytes = sizeof(T) * (size_t)N * L;
   const size_t pbytes = sizeof(double) * 2 * (size_t)chunks * L * (m + 1);
   const size_t hbytes = sizeof(double) * 2 * (size_t)L * (m + 1);
   h->lz.alloc(qbytes + fbytes + pbytes + hbytes * (2 * (m + 1) + 2) + 256);
   char* base = h->lz.as<char>();
-  double2* Q = reinterpret_cast<double2*>(base);
-  double2* F = reinterpret_cast<double2*>(base + qbytes);
+  T* Q = reinterpret_cast<T*>(base);
+  T* F = reinterpret_cast<T*>(base + qbytes);
   double* part = reinterpret_cast<double*>(base + qbytes + fbytes);
   double* hc = reinterpret_cast<double*>(base + qbytes + fbytes + pbytes);         // per pass
   double* alpha_hist = hc + 2 * L * (m + 1);                                        // (m+1) x L x 2
   double* beta_hist = alpha_hist + 2 * (size_t)L * (m + 1);                         // (m+1) x L x 2
 
   h->scratch.alloc(skinny_work_bytes((int)g.rows.len, (int)g.cols.len, std::min(L, 8)) + 256);
-  auto dots_into = [&](const double2* X, int nk, const double2* Y, double* out) {
+  auto dots_into = [&](const T* X, int nk, const T* Y, double* out) {
     const int ncols = nk * L;
-    k_proj_p1<<<dim3(ncols, chunks), 256, 0, st>>>(X, N, L, nk, Y, chunks, part);
+    k_proj_p1<T><<<dim3(ncols, chunks), 256, 0, st>>>(X, N, L, nk, Y, chunks, part);
     CHASE_CHECK_LAUNCH();
     k_proj_p2<<<(ncols + 127) / 128, 128, 0, st>>>(part, chunks, ncols, out);
     CHASE_CHECK_LAUNCH();
@@ -155,17 +157,21 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
   // start block: counter-based generator, stream 1, normalised
   random_block(h, Q, N, N, 0, 0, L, h->opt.seed_lanczos, 1);
   dots_into(Q, 1, Q, hc);
-  k_normalize<<<eblocks, 256, 0, st>>>(Q, N, L, hc, Q);
+  k_normalize<T><<<eblocks, 256, 0, st>>>(Q, N, L, hc, Q);
   CHASE_CHECK_LAUNCH();
 
   for (int j = 0; j < m; ++j) {
-    double2* Qj = Q + (size_t)j * N * L;
+    T* Qj = Q + (size_t)j * N * L;
     // F = H Q_j  (rows of block i from this shard; world sum assembles the full vectors)
     CHASE_CUDA(cudaMemsetAsync(F, 0, fbytes, st));
     if (L == 1 || L == 2 || L == 3 || L == 4 || L == 8) {
       // HBM-bound skinny product: streams the shard once per step
-      zgemm_skinny((int)g.rows.len, L, (int)g.cols.len, hsign, H, ldh, Qj + g.cols.start, N,
-                   F + g.rows.start, N, h->scratch.p, st);
+      if (SC<T>::is_complex)
+        zgemm_skinny((int)g.rows.len, L, (int)g.cols.len, hsign, H, ldh, Qj + g.cols.start, N,
+                     F + g.rows.start, N, h->scratch.p, st);
+      else
+        dgemm_skinny((int)g.rows.len, L, (int)g.cols.len, hsign, H, ldh, Qj + g.cols.start, N,
+                     F + g.rows.start, N, h->scratch.p, st);
     } else {
       ZgemmDesc d;
       d.M = (int)g.rows.len; d.N = L; d.K = (int)g.cols.len;
@@ -173,22 +179,22 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
       d.B = Qj + g.cols.start; d.ldb = N;
       d.C = F + g.rows.start; d.ldc = N;
       d.alpha = hsign; d.beta = 0.0;
-      zgemm(d, st);
+      gemm(h, d);
     }
-    allreduce_doubles(h, h->world, h->world_size, reinterpret_cast<double*>(F), 2 * (size_t)N * L);
+    allreduce_doubles(h, h->world, h->world_size, reinterpret_cast<double*>(F), SC<T>::ND * (size_t)N * L);
     // two classical Gram-Schmidt passes against Q_0..Q_j (full reorthogonalisation); the first
     // pass's coefficient on Q_j is alpha_j = Re(q_j^H H q_j)
     dots_into(Q, j + 1, F, hc);
     CHASE_CUDA(cudaMemcpyAsync(alpha_hist + 2 * (size_t)j * L, hc + 2 * (size_t)j * L, sizeof(double) * 2 * L,
                                cudaMemcpyDeviceToDevice, st));
-    k_proj_sub<<<eblocks, 256, 0, st>>>(Q, N, L, j + 1, hc, F);
+    k_proj_sub<T><<<eblocks, 256, 0, st>>>(Q, N, L, j + 1, hc, F);
     CHASE_CHECK_LAUNCH();
     dots_into(Q, j + 1, F, hc);
-    k_proj_sub<<<eblocks, 256, 0, st>>>(Q, N, L, j + 1, hc, F);
+    k_proj_sub<T><<<eblocks, 256, 0, st>>>(Q, N, L, j + 1, hc, F);
     CHASE_CHECK_LAUNCH();
-    double2* dn = reinterpret_cast<double2*>(beta_hist) + (size_t)j * L;
-    dots_into(F, 1, F, reinterpret_cast<double*>(dn));
-    k_normalize<<<eblocks, 256, 0, st>>>(F, N, L, reinterpret_cast<double*>(dn), Q + (size_t)(j + 1) * N * L);
+    double* dn = beta_hist + 2 * (size_t)j * L;
+    dots_into(F, 1, F, dn);
+    k_normalize<T><<<eblocks, 256, 0, st>>>(F, N, L, dn, Q + (size_t)(j + 1) * N * L);
     CHASE_CHECK_LAUNCH();
   }
   std::vector<double> ah(2 * (size_t)L * m), bh(2 * (size_t)L * m);
@@ -208,15 +214,15 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
       if (j + 1 < m && b <= 1e-14 * std::max(1.0, std::fabs(a))) break;   // invariant subspace
     }
     const int k = (int)al.size();
-    std::vector<double> T((size_t)k * k, 0.0), Z;
+    std::vector<double> Tm((size_t)k * k, 0.0), Z;
     for (int i = 0; i < k; ++i) {
-      T[(size_t)i * k + i] = al[i];
-      if (i + 1 < k) T[(size_t)i * k + i + 1] = T[(size_t)(i + 1) * k + i] = be[i];
+      Tm[(size_t)i * k + i] = al[i];
+      if (i + 1 < k) Tm[(size_t)i * k + i + 1] = Tm[(size_t)(i + 1) * k + i] = be[i];
     }
-    host_syev(k, T, Z);
+    host_syev(k, Tm, Z);
     double thmax = -INFINITY;
     for (int i = 0; i < k; ++i) {
-      const double th = T[(size_t)i * k + i];
+      const double th = Tm[(size_t)i * k + i];
       thmax = std::max(thmax, th);
       ritz.push_back(th);
       wts.push_back(Z[i] * Z[i] / L);          // |z_1i|^2 / L (first row of Z)
@@ -242,6 +248,10 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
   for (double t : ritz) nu = std::max(nu, std::fabs(t));
   o.nu = nu;
   return o;
+}
+
+LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e) {
+  return h->real() ? lanczos_t<double>(h, H, ldh, n_e) : lanczos_t<double2>(h, H, ldh, n_e);
 }
 
 }  // namespace chase

@@ -24,6 +24,7 @@
 #include "dense.h"
 #include "handle.h"
 #include "linalg.h"
+#include "scalar.cuh"
 
 namespace chase {
 
@@ -61,10 +62,56 @@ struct PhaseTimer {
   }
 };
 
+// Small n x n factorizations: the complex path runs them directly; the real-symmetric path (f2)
+// runs the same complex kernels on a complexified copy (the matrices stay real through them).
+// G: Gram (upper triangle) on entry; on exit `Rinv` holds R^{-1} in the element type.
+template <class T>
+bool chol_and_inverse(void* G, void* G2, void* Z, int n, int* d_info, cudaStream_t st, void** Rinv);
+
+template <>
+bool chol_and_inverse<double2>(void* G, void* G2, void* Z, int n, int* d_info, cudaStream_t st, void** Rinv) {
+  if (!cholesky_upper(G, n, n, d_info, st)) return false;
+  trinv_upper(G, n, G2, n, Z, n, st);
+  *Rinv = G2;
+  return true;
+}
+
+template <>
+bool chol_and_inverse<double>(void* G, void* G2, void* Z, int n, int* d_info, cudaStream_t st, void** Rinv) {
+  double2* Gc = reinterpret_cast<double2*>(G2);
+  real_to_complex(Gc, n, reinterpret_cast<const double*>(G), n, n, n, st);
+  if (!cholesky_upper(Gc, n, n, d_info, st)) return false;
+  trinv_upper(Gc, n, Z, n, G, n, st);                          // G reused as scratch (n x 64 complex)
+  complex_to_real(reinterpret_cast<double*>(G), n, reinterpret_cast<const double2*>(Z), n, n, n, st);
+  *Rinv = G;
+  return true;
+}
+
+// Rayleigh-Ritz eigensolver: G (n x n Hermitian / symmetric, destroyed) -> theta, eigenvectors in *Zout
+template <class T>
+void rr_eig(void* G, void* G2, void* Z, int n, double* theta, cudaStream_t st, void** Zout);
+
+template <>
+void rr_eig<double2>(void* G, void*, void* Z, int n, double* theta, cudaStream_t st, void** Zout) {
+  heev_jacobi(G, n, n, theta, Z, n, st);
+  *Zout = Z;
+}
+
+template <>
+void rr_eig<double>(void* G, void* G2, void* Z, int n, double* theta, cudaStream_t st, void** Zout) {
+  double2* Gc = reinterpret_cast<double2*>(G2);
+  real_to_complex(Gc, n, reinterpret_cast<const double*>(G), n, n, n, st);
+  heev_jacobi(Gc, n, n, theta, Z, n, st);                       // real rotations: Z stays real
+  complex_to_real(reinterpret_cast<double*>(G), n, reinterpret_cast<const double2*>(Z), n, n, n, st);
+  *Zout = G;
+}
+
 }  // namespace
 
-chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int nex, int deg, double tol,
-                   double* ritz_values, void* ritz_vectors, int64_t ldv_out, chase_report* rep) {
+template <class T>
+static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int nev, int nex, int deg, double tol,
+                            double* ritz_values, void* ritz_vectors, int64_t ldv_out, chase_report* rep) {
+  constexpr int ND = SC<T>::ND;
   const Grid& g = h->grid;
   const int64_t p = g.rows.len, q = g.cols.len, r0 = g.rows.start, c0 = g.cols.start;
   const Range I = g.diag();
@@ -73,13 +120,13 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
   const bool largest = h->opt.largest;
   const int deg_max = h->opt.deg_max;
 
-  double2* V = h->V.as<double2>();
-  double2* V2 = h->V2.as<double2>();
-  double2* W = h->W.as<double2>();
-  double2* HV = h->HV.as<double2>();
-  double2* G = h->G.as<double2>();
-  double2* G2 = h->G2.as<double2>();
-  double2* Z = h->Z.as<double2>();
+  T* V = h->V.as<T>();
+  T* V2 = h->V2.as<T>();
+  T* W = h->W.as<T>();
+  T* HV = h->HV.as<T>();
+  T* G = h->G.as<T>();
+  T* G2 = h->G2.as<T>();
+  T* Z = h->Z.as<T>();
   // scratch: reduction partials | theta | res2 | perm | info
   const size_t red_doubles = colreduce_scratch(n_e);
   h->red.alloc(sizeof(double) * (red_doubles + 2 * (size_t)n_e) + sizeof(int) * ((size_t)n_e + 8));
@@ -102,7 +149,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
 
   // ---- initial V-hat (Require of Alg. 1)
   if (h->opt.approx)
-    zcopy2d(V, q, ritz_vectors, ldv_out, q, n_e, st);
+    copy2d<T>(V, q, ritz_vectors, ldv_out, q, n_e, st);
   else
     random_block(h, V, q, q, c0, 0, n_e, h->opt.seed_v, 0);
 
@@ -115,9 +162,9 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
   while (locked < nev && it < h->opt.max_iter) {                // line 3
     ++it;
     const int n_act = n_e - locked;
-    double2* Va = V + (int64_t)locked * q;
-    double2* Wa = W + (int64_t)locked * p;
-    double2* HVa = HV + (int64_t)locked * p;
+    T* Va = V + (int64_t)locked * q;
+    T* Wa = W + (int64_t)locked * p;
+    T* HVa = HV + (int64_t)locked * p;
 
     // ---- line 4: Filter
     t_f.start(st);
@@ -131,14 +178,14 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
       d.use3m = h->opt.gemm3m;
       d.M = locked; d.N = n_act; d.K = (int)q; d.conjA = true;
       d.A = V; d.lda = q; d.B = Va; d.ldb = q; d.C = G2; d.ldc = locked;
-      zgemm(d, st);
-      allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G2), 2 * (size_t)locked * n_act);
+      gemm(h, d);
+      allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G2), ND * (size_t)locked * n_act);
       ZgemmDesc e;                                  // Va -= Y T
       e.use3m = h->opt.gemm3m;
       e.M = (int)q; e.N = n_act; e.K = locked;
       e.A = V; e.lda = q; e.B = G2; e.ldb = locked; e.C = Va; e.ldc = q;
       e.alpha = -1.0; e.beta = 1.0;
-      zgemm(e, st);
+      gemm(h, e);
     }
     int cholqr_passes = 2;
     for (int pass = 0; pass < cholqr_passes; ++pass) {
@@ -148,34 +195,34 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
         d.M = n_act; d.N = n_act; d.K = (int)q; d.conjA = true;
         d.upper_only = true;                        // Cholesky reads the upper triangle only
         d.A = Va; d.lda = q; d.B = Va; d.ldb = q; d.C = G; d.ldc = n_act;
-        zgemm(d, st);
-        allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G), 2 * (size_t)n_act * n_act);
+        gemm(h, d);
+        allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G), ND * (size_t)n_act * n_act);
       };
       gram();
-      if (!cholesky_upper(G, n_act, n_act, d_info, st)) {
+      void* Rinv = nullptr;
+      if (!chol_and_inverse<T>(G, G2, Z, n_act, d_info, st, &Rinv)) {
         // shifted CholQR (Fukaya et al.): G + s I with s = 11 (N n + n(n+1)) u ||G||, then two
         // more unshifted passes (CholQR3)
         gram();
-        std::vector<double2> dg(n_act);
-        CHASE_CUDA(cudaMemcpy2DAsync(dg.data(), sizeof(double2), G, sizeof(double2) * (n_act + 1),
-                                     sizeof(double2), n_act, cudaMemcpyDeviceToHost, st));
+        std::vector<T> dg(n_act);
+        CHASE_CUDA(cudaMemcpy2DAsync(dg.data(), sizeof(T), G, sizeof(T) * (n_act + 1), sizeof(T), n_act,
+                                     cudaMemcpyDeviceToHost, st));
         CHASE_CUDA(cudaStreamSynchronize(st));
         double trace = 0.0;
-        for (auto& v : dg) trace += v.x;
+        for (auto& v : dg) trace += SC<T>::re(v);
         const double s = 11.0 * ((double)g.N * n_act + (double)n_act * (n_act + 1)) * 1.1102230246251565e-16 * trace;
-        add_diag(G, n_act, n_act, s, st);
-        if (!cholesky_upper(G, n_act, n_act, d_info, st))
+        add_diag<T>(G, n_act, n_act, s, st);
+        if (!chol_and_inverse<T>(G, G2, Z, n_act, d_info, st, &Rinv))
           throw NumericError("CholQR failed even with the shifted fallback");
         cholqr_passes = 3;
       }
-      trinv_upper(G, n_act, G2, n_act, Z, n_act, st);
       ZgemmDesc d;                                  // V2 = Va R^{-1}
       d.use3m = h->opt.gemm3m;
       d.M = (int)q; d.N = n_act; d.K = n_act;
       d.b_upper = true;                             // R^{-1} is upper triangular
-      d.A = Va; d.lda = q; d.B = G2; d.ldb = n_act; d.C = V2; d.ldc = q;
-      zgemm(d, st);
-      zcopy2d(Va, q, V2, q, q, n_act, st);
+      d.A = Va; d.lda = q; d.B = Rinv; d.ldb = n_act; d.C = V2; d.ldc = q;
+      gemm(h, d);
+      copy2d<T>(Va, q, V2, q, q, n_act, st);
     }
     t_qr.stop(st);
 
@@ -189,32 +236,33 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
       d.A = Va + (I.start - c0); d.lda = q;
       d.B = HVa + (I.start - r0); d.ldb = p;
       d.C = G; d.ldc = n_act;
-      zgemm(d, st);
+      gemm(h, d);
     } else {
-      zzero2d(G, n_act, n_act, n_act, st);
+      zero2d<T>(G, n_act, n_act, n_act, st);
     }
-    allreduce_doubles(h, h->world, h->world_size, reinterpret_cast<double*>(G), 2 * (size_t)n_act * n_act);
-    hermitize(G, n_act, n_act, st);
-    heev_jacobi(G, n_act, n_act, d_theta, Z, n_act, st);
+    allreduce_doubles(h, h->world, h->world_size, reinterpret_cast<double*>(G), ND * (size_t)n_act * n_act);
+    hermitize<T>(G, n_act, n_act, st);
+    void* Zr = nullptr;
+    rr_eig<T>(G, G2, Z, n_act, d_theta, st, &Zr);
     {
       ZgemmDesc d;                                  // V <- Q Z
       d.use3m = h->opt.gemm3m;
       d.M = (int)q; d.N = n_act; d.K = n_act;
-      d.A = Va; d.lda = q; d.B = Z; d.ldb = n_act; d.C = V2; d.ldc = q;
-      zgemm(d, st);
-      zcopy2d(Va, q, V2, q, q, n_act, st);
+      d.A = Va; d.lda = q; d.B = Zr; d.ldb = n_act; d.C = V2; d.ldc = q;
+      gemm(h, d);
+      copy2d<T>(Va, q, V2, q, q, n_act, st);
       ZgemmDesc e;                                  // HV <- (HQ) Z   (into W, then swap roles)
       e.use3m = h->opt.gemm3m;
       e.M = (int)p; e.N = n_act; e.K = n_act;
-      e.A = HVa; e.lda = p; e.B = Z; e.ldb = n_act; e.C = Wa; e.ldc = p;
-      zgemm(e, st);
+      e.A = HVa; e.lda = p; e.B = Zr; e.ldb = n_act; e.C = Wa; e.ldc = p;
+      gemm(h, e);
     }
     t_rr.stop(st);
 
     // ---- line 7: residuals  ||H v - theta v|| over I_ij, summed over the world
     t_res.start(st);
     if (I.len > 0)
-      resid_norms2(Wa + (I.start - r0), p, Va + (I.start - c0), q, d_theta, I.len, n_act, d_res2, part, st);
+      resid_norms2<T>(Wa + (I.start - r0), p, Va + (I.start - c0), q, d_theta, I.len, n_act, d_res2, part, st);
     else
       CHASE_CUDA(cudaMemsetAsync(d_res2, 0, sizeof(double) * n_act, st));
     allreduce_doubles(h, h->world, h->world_size, d_res2, n_act);
@@ -255,8 +303,8 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     }
     for (int a = 0; a < na; ++a) { ritz[locked + a] = rz[a]; res[locked + a] = rs[a]; }
     CHASE_CUDA(cudaMemcpyAsync(d_perm, perm.data(), sizeof(int) * na, cudaMemcpyHostToDevice, st));
-    permute_cols(V2, q, V + (int64_t)locked * q, q, q, d_perm, na, st);
-    zcopy2d(V + (int64_t)locked * q, q, V2, q, q, na, st);
+    permute_cols<T>(V2, q, V + (int64_t)locked * q, q, q, d_perm, na, st);
+    copy2d<T>(V + (int64_t)locked * q, q, V2, q, q, na, st);
     CHASE_CUDA(cudaStreamSynchronize(st));   // perm (host) goes out of scope
   }
 
@@ -274,7 +322,7 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     max_resid = std::max(max_resid, res[src]);
   }
   CHASE_CUDA(cudaMemcpyAsync(d_perm, out_cols.data(), sizeof(int) * nev, cudaMemcpyHostToDevice, st));
-  permute_cols(ritz_vectors, ldv_out, V, q, q, d_perm, nev, st);
+  permute_cols<T>(ritz_vectors, ldv_out, V, q, q, d_perm, nev, st);
   t_all.stop(st);
   CHASE_CUDA(cudaStreamSynchronize(st));
   t_all.collect();
@@ -301,6 +349,13 @@ chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int ne
     return CHASE_E_MAXITER;
   }
   return CHASE_OK;
+}
+
+chase_status solve(chase_handle* h, const void* Hv, int64_t ldh, int nev, int nex, int deg, double tol,
+                   double* ritz_values, void* ritz_vectors, int64_t ldv_out, chase_report* rep) {
+  if (h->real())
+    return solve_t<double>(h, Hv, ldh, nev, nex, deg, tol, ritz_values, ritz_vectors, ldv_out, rep);
+  return solve_t<double2>(h, Hv, ldh, nev, nex, deg, tol, ritz_values, ritz_vectors, ldv_out, rep);
 }
 
 }  // namespace chase

@@ -219,3 +219,112 @@ void zgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda,
   CHASE_CHECK_LAUNCH();
 }
 }  // namespace chase
+
+// ------------------------------------------------------------------ real (f2) GEMM launcher
+#include "dgemm.cuh"
+namespace chase {
+template <bool TRANS>
+static void launch_d(const ZgemmDesc& d, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    CHASE_CUDA(cudaFuncSetAttribute(dgemm_dmma_kernel<TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)DCfg::SMEM));
+    attr_set = true;
+  }
+  DgemmParams p;
+  p.M = d.M; p.N = d.N; p.K = d.K;
+  p.alpha = d.alpha; p.beta = d.beta; p.gamma = d.gamma;
+  p.A = reinterpret_cast<const double*>(d.A); p.lda = d.lda;
+  p.B = reinterpret_cast<const double*>(d.B); p.ldb = d.ldb;
+  p.S = reinterpret_cast<const double*>(d.S); p.lds = d.lds;
+  p.shift_lo = d.shift_lo; p.shift_hi = d.shift_hi; p.shift_off = d.shift_off;
+  p.C = reinterpret_cast<double*>(d.C); p.ldc = d.ldc;
+  p.upper_only = d.upper_only ? 1 : 0;
+  p.b_upper = d.b_upper ? 1 : 0;
+  const int grid = ceil_div(d.M, DCfg::BM) * ceil_div(d.N, DCfg::BN);
+  dgemm_dmma_kernel<TRANS><<<grid, DCfg::THREADS, DCfg::SMEM, st>>>(p);
+  CHASE_CHECK_LAUNCH();
+}
+
+void dgemm(const ZgemmDesc& d0, cudaStream_t st) {
+  if (d0.M <= 0 || d0.N <= 0) return;
+  if (d0.K <= 0) throw CudaError("dgemm: K must be > 0");
+  ZgemmDesc d = d0;
+  if (!d.S) d.shift_lo = d.shift_hi = 0;
+  if (d.conjA) launch_d<true>(d, st); else launch_d<false>(d, st);
+}
+}  // namespace chase
+
+// ------------------------------------------------------------------ real skinny (Lanczos, f2)
+namespace chase {
+namespace {
+template <int L>
+__global__ void __launch_bounds__(SK_T) k_skinny_real(int M, int K, int kchunk, const double* __restrict__ A,
+                                                      int64_t lda, const double* __restrict__ B, int64_t ldb,
+                                                      double* __restrict__ P) {
+  __shared__ double Bs[SK_KB][L];
+  const int m = blockIdx.x * SK_T + threadIdx.x;
+  const int k0 = blockIdx.y * kchunk, k1 = min(K, k0 + kchunk);
+  double ar[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) ar[l] = 0.0;
+  for (int kb = k0; kb < k1; kb += SK_KB) {
+    const int kn = min(SK_KB, k1 - kb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < SK_KB * L; e += SK_T) {
+      const int kk = e % SK_KB, l = e / SK_KB;
+      Bs[kk][l] = kk < kn ? B[(int64_t)(kb + kk) + (int64_t)l * ldb] : 0.0;
+    }
+    __syncthreads();
+    if (m < M) {
+      const double* a = A + m + (int64_t)kb * lda;
+#pragma unroll 4
+      for (int kk = 0; kk < kn; ++kk) {
+        const double h = __ldg(a + (int64_t)kk * lda);
+#pragma unroll
+        for (int l = 0; l < L; ++l) ar[l] = fma(h, Bs[kk][l], ar[l]);
+      }
+    }
+  }
+  if (m < M) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) P[((int64_t)blockIdx.y * L + l) * M + m] = ar[l];
+  }
+}
+
+__global__ void k_skinny_reduce_real(int M, int L, int splits, double alpha, const double* __restrict__ P,
+                                     double* __restrict__ C, int64_t ldc) {
+  const int64_t total = (int64_t)M * L;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i % M), l = (int)(i / M);
+    double r = 0.0;
+    for (int s = 0; s < splits; ++s) r += P[((int64_t)s * L + l) * M + m];
+    C[m + (int64_t)l * ldc] = alpha * r;
+  }
+}
+}  // namespace
+
+void dgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
+                  void* C, int64_t ldc, void* work, cudaStream_t st) {
+  if (M <= 0 || L <= 0) return;
+  const int splits = skinny_splits(M, K);
+  const int kchunk = ceil_div(K, splits);
+  dim3 grid(ceil_div(M, SK_T), splits);
+  auto* Ad = reinterpret_cast<const double*>(A);
+  auto* Bd = reinterpret_cast<const double*>(B);
+  auto* P = reinterpret_cast<double*>(work);
+  switch (L) {
+    case 1: k_skinny_real<1><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 2: k_skinny_real<2><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 3: k_skinny_real<3><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 4: k_skinny_real<4><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 8: k_skinny_real<8><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    default: throw CudaError("dgemm_skinny: L must be 1, 2, 3, 4 or 8");
+  }
+  CHASE_CHECK_LAUNCH();
+  const int64_t total = (int64_t)M * L;
+  k_skinny_reduce_real<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(
+      M, L, splits, alpha, P, reinterpret_cast<double*>(C), ldc);
+  CHASE_CHECK_LAUNCH();
+}
+}  // namespace chase

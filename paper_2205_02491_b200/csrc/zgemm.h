@@ -21,6 +21,8 @@ struct ZgemmDesc {
 
 // C = alpha*op(A)*B - alpha*gamma*S[shift rows] + beta*C   (all complex double, column-major)
 void zgemm(const ZgemmDesc& d, cudaStream_t st);
+// The same contract for real double (op(A) = A^T when conjA; use3m ignored).  Real-symmetric f2.
+void dgemm(const ZgemmDesc& d, cudaStream_t st);
 
 }  // namespace chase
 
@@ -29,5 +31,8 @@ namespace chase {
 // used by the Lanczos step).  `work` must hold skinny_work_bytes(M, K, L).
 size_t skinny_work_bytes(int M, int K, int L);
 void zgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B,
+                  int64_t ldb, void* C, int64_t ldc, void* work, cudaStream_t st);
+// real variant (f2); `work` as for the complex one (it needs half of it)
+void dgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B,
                   int64_t ldb, void* C, int64_t ldc, void* work, cudaStream_t st);
 }  // namespace chase

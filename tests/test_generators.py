@@ -95,3 +95,17 @@ def test_block_partition_remainder_rule():
     assert block_partition(9, 3) == [(0, 3), (3, 3), (6, 3)]
     parts = block_partition(1001, 4)
     assert sum(l for _, l in parts) == 1001 and parts[-1][0] + parts[-1][1] == 1001
+
+
+@pytest.mark.parametrize("kind", ["r1", "r2"])
+@pytest.mark.parametrize("fam", ["uniform", "121", "wilkinson"])
+def test_real_generators_spectrum_and_eigenvectors(kind, fam):
+    """Real-symmetric inputs (f2): symmetric, exact spectrum (brute-force Jacobi), exact eigenvectors."""
+    M = make_matrix(fam, 40, kind, seed=6)
+    H = M.dense()
+    assert H.dtype == np.float64 and np.max(np.abs(H - H.T)) <= 1e-15 * np.max(np.abs(M.lam))
+    np.testing.assert_allclose(jacobi_eigvalsh(H), M.lam, atol=1e-13 * np.max(np.abs(M.lam)))
+    idx = np.arange(0, 40, 3)
+    X = M.eigvecs(idx)
+    assert np.max(np.linalg.norm(H @ X - X * M.lam[idx][None, :], axis=0)) <= 1e-13 * np.max(np.abs(M.lam))
+    np.testing.assert_allclose(X.T @ X, np.eye(len(idx)), atol=1e-13)

@@ -177,3 +177,13 @@ def test_invalid_arguments():
         oracle.chase_solve(H, 8, 5)
     with pytest.raises(ValueError):
         oracle.chase_solve(H, 0, 5)
+
+
+@pytest.mark.parametrize("fam,kind", [("uniform", "r1"), ("121", "r2"), ("wilkinson", "r2")])
+def test_solve_real_symmetric(fam, kind):
+    """Real-symmetric variant (f2; the paper's experimental field): float64 throughout."""
+    M = make_matrix(fam, 301, kind, seed=2)
+    H = M.dense()
+    vals, vecs, rep = oracle.chase_solve(H, 30, 10, tol=1e-10)
+    assert vecs.dtype == np.float64
+    _check_solution(M, vals, vecs, rep, 30, 1e-10, H)
