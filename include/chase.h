@@ -77,7 +77,7 @@ typedef struct {
 typedef struct {
   int32_t iterations, locked;
   int64_t matvecs;                /* sum over filter calls of sum_a m_a (P:729-731 footnote) */
-  double filter_flops;            /* 8 N^2 matvecs (complex) */
+  double filter_flops;            /* 8 N^2 matvecs (complex) or 2 N^2 matvecs (real) */
   double t_all, t_lanczos, t_filter, t_qr, t_rr, t_resid;   /* seconds, Table 2 columns P:646-655 */
   double b_sup, mu_1, mu_ne, nu, max_resid;
 } chase_report;

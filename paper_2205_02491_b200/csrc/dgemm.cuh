@@ -23,7 +23,7 @@ struct DCfg {
   static constexpr int BM = 64 * WM, BN = 32 * WN, BK = 32;
   static constexpr int NWARPS = WM * WN, THREADS = NWARPS * 32;
   static constexpr uint32_t A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8, STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 2 * STAGES * 8 + 1024;
 };
 
 struct DgemmParams {
@@ -41,6 +41,7 @@ struct DgemmParams {
   int64_t ldc;
   int upper_only;
   int b_upper;
+  int a_chunked;        // TMA path: forward A as one 3-D box (M % 16 == 0)
 };
 
 namespace dg {
@@ -62,14 +63,21 @@ __device__ __forceinline__ uint32_t soff(int r, int x) {
 }
 }  // namespace dg
 
-template <bool TRANS_A>
-__global__ void __launch_bounds__(DCfg::THREADS, 1) dgemm_dmma_kernel(DgemmParams p) {
+// USE_TMA: operands 16-byte aligned with even leading dimensions -> TMA boxes filled by thread 0
+// into an mbarrier ring (as zgemm.cuh); otherwise cooperative 8-byte cp.async with a
+// __syncthreads ring.  Both produce the identical swizzled shared-memory layout.
+template <bool TRANS_A, bool USE_TMA>
+__global__ void __launch_bounds__(DCfg::THREADS, 1)
+    dgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      DgemmParams p) {
   constexpr int WN = DCfg::WN, STAGES = DCfg::STAGES, BM = DCfg::BM, BN = DCfg::BN, BK = DCfg::BK;
   constexpr int THREADS = DCfg::THREADS;
   constexpr uint32_t A_BYTES = DCfg::A_BYTES, STAGE_BYTES = DCfg::STAGE_BYTES;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int tiles_n = (p.N + BN - 1) / BN;
@@ -123,10 +131,46 @@ __global__ void __launch_bounds__(DCfg::THREADS, 1) dgemm_dmma_kernel(DgemmParam
     }
   };
 
+  auto tma_issue = [&](int kt) {
+    const int s = kt % STAGES;
+    unsigned char* sa = smem + s * STAGE_BYTES;
+    unsigned char* sb = sa + A_BYTES;
+    mbar_arrive_expect_tx(full + s, STAGE_BYTES);
+    const int k0 = kt * BK;
+    if constexpr (!TRANS_A) {
+      if (p.a_chunked) {
+        tma_load_3d(sa, &tmA, 0, k0, m0 / 16, full + s);
+      } else {
 #pragma unroll
-  for (int kt = 0; kt < STAGES - 1; ++kt) {
-    if (kt < KT) stage_load(kt);
-    dg::cp_commit();
+        for (int c = 0; c < BM / 16; ++c) tma_load_2d(sa + c * (BK * 128), &tmA, m0 + 16 * c, k0, full + s);
+      }
+    } else {
+#pragma unroll
+      for (int kc = 0; kc < BK / 16; ++kc) tma_load_2d(sa + kc * (BM * 128), &tmA, k0 + 16 * kc, m0, full + s);
+    }
+#pragma unroll
+    for (int kc = 0; kc < BK / 16; ++kc) tma_load_2d(sb + kc * (BN * 128), &tmB, k0 + 16 * kc, n0, full + s);
+  };
+  if constexpr (USE_TMA) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(full + s, 1);
+        mbar_init(empty + s, DCfg::NWARPS);
+      }
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_prefetch_desc(&tmA);
+      tma_prefetch_desc(&tmB);
+      for (int kt = 0; kt < STAGES - 1 && kt < KT; ++kt) tma_issue(kt);
+    }
+  } else {
+#pragma unroll
+    for (int kt = 0; kt < STAGES - 1; ++kt) {
+      if (kt < KT) stage_load(kt);
+      dg::cp_commit();
+    }
   }
 
   const int wm = warp / WN, wn = warp % WN;
@@ -138,10 +182,18 @@ __global__ void __launch_bounds__(DCfg::THREADS, 1) dgemm_dmma_kernel(DgemmParam
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int kt = 0; kt < KT; ++kt) {
-    dg::cp_wait<STAGES - 2>();
-    __syncthreads();                         // tile kt visible; slot of tile kt-1 free
-    if (kt + STAGES - 1 < KT) stage_load(kt + STAGES - 1);
-    dg::cp_commit();
+    if constexpr (USE_TMA) {
+      if (threadIdx.x == 0 && kt + STAGES - 1 < KT) {
+        if (kt >= 1) mbar_wait(empty + (kt - 1) % STAGES, ((kt - 1) / STAGES) & 1);
+        tma_issue(kt + STAGES - 1);
+      }
+      mbar_wait(full + kt % STAGES, (kt / STAGES) & 1);
+    } else {
+      dg::cp_wait<STAGES - 2>();
+      __syncthreads();                         // tile kt visible; slot of tile kt-1 free
+      if (kt + STAGES - 1 < KT) stage_load(kt + STAGES - 1);
+      dg::cp_commit();
+    }
     const uint32_t sa = smem_base + (kt % STAGES) * STAGE_BYTES;
     const uint32_t sb = sa + A_BYTES;
 #pragma unroll
@@ -165,8 +217,12 @@ __global__ void __launch_bounds__(DCfg::THREADS, 1) dgemm_dmma_kernel(DgemmParam
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) zg::dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
     }
+    if constexpr (USE_TMA) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + kt % STAGES);
+    }
   }
-  dg::cp_wait<0>();
+  if constexpr (!USE_TMA) dg::cp_wait<0>();
 
   const double ag = p.alpha * p.gamma;
 #pragma unroll

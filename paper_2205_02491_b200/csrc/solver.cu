@@ -331,7 +331,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     rep->iterations = it;
     rep->locked = locked;
     rep->matvecs = matvecs;
-    rep->filter_flops = 8.0 * (double)g.N * (double)g.N * (double)matvecs;
+    rep->filter_flops = (SC<T>::is_complex ? 8.0 : 2.0) * (double)g.N * (double)g.N * (double)matvecs;
     rep->t_all = t_all.total_ms * 1e-3;
     rep->t_lanczos = t_lz.total_ms * 1e-3;
     rep->t_filter = t_f.total_ms * 1e-3;

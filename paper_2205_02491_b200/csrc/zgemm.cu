@@ -223,13 +223,50 @@ void zgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda,
 // ------------------------------------------------------------------ real (f2) GEMM launcher
 #include "dgemm.cuh"
 namespace chase {
-template <bool TRANS>
+// Real tensor maps: dim 0 = rows (doubles, contiguous), dim 1 = cols; box {16 doubles, box_cols}.
+static void make_dmatrix_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                              int box_cols) {
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {16u, (cuuint32_t)box_cols};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = get_encode()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (real) failed");
+}
+
+static bool make_dmatrix_tmap_chunked(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                                      int box_cols, int box_chunks) {
+  if (rows % 16 != 0) return false;
+  cuuint64_t dims[3] = {16u, (cuuint64_t)cols, (cuuint64_t)(rows / 16)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 8), 128u};
+  cuuint32_t box[3] = {16u, (cuuint32_t)box_cols, (cuuint32_t)box_chunks};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = get_encode()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool TRANS, bool TMA>
 static void launch_d(const ZgemmDesc& d, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    CHASE_CUDA(cudaFuncSetAttribute(dgemm_dmma_kernel<TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CHASE_CUDA(cudaFuncSetAttribute(dgemm_dmma_kernel<TRANS, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)DCfg::SMEM));
     attr_set = true;
+  }
+  CUtensorMap ta{}, tb{};
+  bool chunked = false;
+  if (TMA) {
+    if (!TRANS) {
+      chunked = make_dmatrix_tmap_chunked(&ta, d.A, d.M, d.K, d.lda, DCfg::BK, DCfg::BM / 16);
+      if (!chunked) make_dmatrix_tmap(&ta, d.A, d.M, d.K, d.lda, DCfg::BK);
+    } else {
+      make_dmatrix_tmap(&ta, d.A, d.K, d.M, d.lda, DCfg::BM);
+    }
+    make_dmatrix_tmap(&tb, d.B, d.K, d.N, d.ldb, DCfg::BN);
   }
   DgemmParams p;
   p.M = d.M; p.N = d.N; p.K = d.K;
@@ -241,8 +278,9 @@ static void launch_d(const ZgemmDesc& d, cudaStream_t st) {
   p.C = reinterpret_cast<double*>(d.C); p.ldc = d.ldc;
   p.upper_only = d.upper_only ? 1 : 0;
   p.b_upper = d.b_upper ? 1 : 0;
+  p.a_chunked = chunked ? 1 : 0;
   const int grid = ceil_div(d.M, DCfg::BM) * ceil_div(d.N, DCfg::BN);
-  dgemm_dmma_kernel<TRANS><<<grid, DCfg::THREADS, DCfg::SMEM, st>>>(p);
+  dgemm_dmma_kernel<TRANS, TMA><<<grid, DCfg::THREADS, DCfg::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();
 }
 
@@ -251,7 +289,14 @@ void dgemm(const ZgemmDesc& d0, cudaStream_t st) {
   if (d0.K <= 0) throw CudaError("dgemm: K must be > 0");
   ZgemmDesc d = d0;
   if (!d.S) d.shift_lo = d.shift_hi = 0;
-  if (d.conjA) launch_d<true>(d, st); else launch_d<false>(d, st);
+  // TMA needs 16-byte aligned bases and leading dimensions that are a multiple of 16 bytes
+  const bool tma = (reinterpret_cast<uintptr_t>(d.A) % 16 == 0) && (reinterpret_cast<uintptr_t>(d.B) % 16 == 0) &&
+                   (d.lda % 2 == 0) && (d.ldb % 2 == 0);
+  if (d.conjA) {
+    if (tma) launch_d<true, true>(d, st); else launch_d<true, false>(d, st);
+  } else {
+    if (tma) launch_d<false, true>(d, st); else launch_d<false, false>(d, st);
+  }
 }
 }  // namespace chase
 

@@ -5,21 +5,23 @@ import numpy as np
 import torch
 sys.path.insert(0, ".")
 import paper_2205_02491_b200 as pkg
-from chase_gen.dense import G2Matrix
+from chase_gen.dense import G2Matrix, R2Matrix
 from chase_gen.spectra import spectrum
-from chase_gen.device import DeviceG2
+from chase_gen.device import device_matrix
 
 N, nev, nex = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 fam = sys.argv[4] if len(sys.argv) > 4 else "uniform"
-M = G2Matrix(spectrum(fam, N), seed=1)
-H = torch.empty((N, N), dtype=torch.complex128, device="cuda").t()
-DeviceG2(M).fill(H, 0, 0)
-ch = pkg.Chase(N, nev, nex)
+real = len(sys.argv) > 6 and sys.argv[6] == "r64"
+M = (R2Matrix if real else G2Matrix)(spectrum(fam, N), seed=1)
+H = torch.empty((N, N), dtype=torch.float64 if real else torch.complex128, device="cuda").t()
+device_matrix(M).fill(H, 0, 0)
+ch = pkg.Chase(N, nev, nex, dtype="r64" if real else "c128")
 ch.set_option("max_iter", int(sys.argv[5]) if len(sys.argv) > 5 else 100)
 vals, vecs, rep, st = ch.solve(H, nev, nex, deg=20, tol=1e-10)
 normH = np.max(np.abs(M.lam))
 print(json.dumps({"N": N, "nev": nev, "nex": nex, "family": fam, "status": st, "t_all": rep["t_all"],
                   "iterations": rep["iterations"], "matvecs": rep["matvecs"],
                   "phases": {k: rep[k] for k in ("t_lanczos", "t_filter", "t_qr", "t_rr", "t_resid")},
+                  "dtype": "r64" if real else "c128",
                   "filter_tflops": rep["filter_flops"] / max(rep["t_filter"], 1e-12) / 1e12,
                   "eig_err_rel": float(np.max(np.abs(vals - M.lam[:nev])) / normH)}))
