@@ -29,19 +29,21 @@ def main():
     dist.init_process_group("gloo")
     grid = grid_shape(world)
     N, nev, nex = int(os.environ.get("MG_N", "1201")), 40, 20
-    M = make_matrix("wilkinson", N, "g2", seed=3)
+    real = os.environ.get("MG_DTYPE", "c128") == "r64"
+    M = make_matrix("wilkinson", N, "r2" if real else "g2", seed=3)
     H = M.dense()
     r0, p, c0, q = shard(N, grid, rank)
     nid = broadcast_nccl_id(rank)
-    ch = pkg.Chase(N, nev, nex, grid=grid, rank=rank, world_size=world, nccl_id=nid, device=local)
+    ch = pkg.Chase(N, nev, nex, grid=grid, rank=rank, world_size=world, nccl_id=nid, device=local,
+                   dtype="r64" if real else "c128")
     assert ch.local_layout() == (r0, p, c0, q)
     dH = dev(H[r0:r0 + p, c0:c0 + q])
     ok = True
     out = []
     rng = np.random.default_rng(0)
     n = 37
-    X = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
-    Y0 = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
+    X = rng.standard_normal((N, n)) + (0 if real else 1j) * rng.standard_normal((N, n))
+    Y0 = rng.standard_normal((N, n)) + (0 if real else 1j) * rng.standard_normal((N, n))
     ref = oracle.hemm_step(H, X, Y0, 0.7, -0.3, 0.45)
     # forward: X V-layout (rows c0..), Y W-layout (rows r0..)
     dY = dev(Y0[r0:r0 + p])
@@ -53,8 +55,10 @@ def main():
     # filter
     degrees = np.sort(np.array([0, 2, 4, 8, 12, 20, 20, 36] + [20] * 20))
     V = oracle.random_block(9, 0, N, 0, len(degrees), 0)
+    V = V.real.copy() if real else V
     dV = dev(V[c0:c0 + q])
-    dW = torch.zeros((len(degrees), p), dtype=torch.complex128, device="cuda").t()
+    dt = torch.float64 if real else torch.complex128
+    dW = torch.zeros((len(degrees), p), dtype=dt, device="cuda").t()
     b_sup, mu_1, mu_ne = M.lam[-1] * 1.01, M.lam[0], M.lam[60]
     mv = ch.filter(dH, dV, dW, degrees, b_sup, mu_1, mu_ne)
     fref, _ = oracle.chebyshev_filter(H, V, degrees, b_sup, mu_1, mu_ne)
@@ -62,8 +66,9 @@ def main():
     # pipelined filter (column chunks, all-reduce overlapped with the next chunk's GEMM)
     degrees2 = np.sort(np.concatenate([np.full(300, 8), np.full(500, 20), np.array([2, 4, 36, 36])]))
     V2 = oracle.random_block(11, 0, N, 0, len(degrees2), 0)
+    V2 = V2.real.copy() if real else V2
     dV2 = dev(V2[c0:c0 + q])
-    dW2 = torch.zeros((len(degrees2), p), dtype=torch.complex128, device="cuda").t()
+    dW2 = torch.zeros((len(degrees2), p), dtype=dt, device="cuda").t()
     ch.filter(dH, dV2, dW2, degrees2, b_sup, mu_1, mu_ne)
     fref2, _ = oracle.chebyshev_filter(H, V2, degrees2, b_sup, mu_1, mu_ne)
     e_filt2 = np.linalg.norm(dV2.cpu().numpy() - fref2[c0:c0 + q]) / np.linalg.norm(fref2[c0:c0 + q])
@@ -80,7 +85,7 @@ def main():
     dist.all_gather_object(all_errs, (errs, vals.tolist(), st, rep["iterations"]))
     if rank == 0:
         normH = np.max(np.abs(M.lam))
-        full = np.zeros((N, nev), dtype=complex)
+        full = np.zeros((N, nev), dtype=float if real else complex)
         for (rr0, pp, cc0, qq, vl, i) in parts:
             if i == 0:
                 full[cc0:cc0 + qq] = vl
@@ -88,7 +93,7 @@ def main():
         e_eig = np.max(np.abs(np.array(vals) - M.lam[:nev])) / normH
         ov, _, orep = oracle.chase_solve(H, nev, nex, deg=20, tol=1e-10)
         same_vals = all(np.array_equal(np.array(a[1]), np.array(all_errs[0][1])) for a in all_errs)
-        line = {"world": world, "grid": f"{grid[0]}x{grid[1]}", "N": N,
+        line = {"world": world, "grid": f"{grid[0]}x{grid[1]}", "N": N, "dtype": "r64" if real else "c128",
                 "max_step_rel_err": max(max(a[0]["fwd"], a[0]["bwd"]) for a in all_errs),
                 "max_filter_rel_err": max(a[0]["filter"] for a in all_errs),
                 "solve_status": [a[2] for a in all_errs], "iterations": [a[3] for a in all_errs],
