@@ -53,7 +53,9 @@ typedef enum {
 
 typedef enum {
   CHASE_C128 = 0, /* complex<double>, interleaved (re, im): Hermitian H -- the north_star path */
-  CHASE_C64 = 1,  /* reserved (complex single) */
+  CHASE_C64 = 1,  /* complex<float> interleaved: Hermitian H in complex single; the filter runs on
+                     the tcgen05 tensor cores (TF32 with the 3xTF32 split).  Round 1: chase_filter
+                     and chase_hemm_step only (1 x c grids for the filter). */
   CHASE_R64 = 2   /* double: real symmetric H, the paper's own experimental field.
                      Every buffer argument is then real double with the same layouts. */
 } chase_dtype;

@@ -101,7 +101,7 @@ def _ld(t):
 class Chase:
     """One rank's handle.  All collective methods must be called by every rank of the grid."""
 
-    C128, R64 = 0, 2          # chase_dtype: complex Hermitian / real symmetric (f2)
+    C128, C64, R64 = 0, 1, 2  # chase_dtype: complex double / complex single (tcgen05) / real symmetric
 
     def __init__(self, N, nev_max, nex_max, grid=(1, 1), rank=0, world_size=1, nccl_id=None,
                  device=0, stream=None, dtype="c128"):
@@ -110,7 +110,8 @@ class Chase:
         self._id = None
         args = InitArgs()
         self.real = dtype in ("r64", "float64", 2)
-        args.dtype = self.R64 if self.real else self.C128
+        self.single = dtype in ("c64", "complex64", 1)
+        args.dtype = self.R64 if self.real else (self.C64 if self.single else self.C128)
         args.N = int(N)
         args.nev_max, args.nex_max = int(nev_max), int(nex_max)
         args.grid_rows, args.grid_cols = int(grid[0]), int(grid[1])

@@ -1,0 +1,263 @@
+// Complex-single fused filter step on the 5th-generation tensor cores (tcgen05, kind::tf32) with
+// the 3xTF32 split ("c64 uses tcgen05 kind::tf32, 3xTF32 split for FP32 accuracy,
+// with FP32 accumulation").
+//
+// Complex arithmetic is mapped onto real TF32 MMAs through the storage itself (no operand copies
+// of H):
+//   forward  W = H V : A = H viewed as a REAL (2M x K) matrix (complex rows interleaved re/im,
+//            MN-major), B1 = Re V, B2 = Im V (planar K x N, K-major).  D1 = A B1, D2 = A B2 hold
+//            (Hr Vr, Hi Vr) and (Hr Vi, Hi Vi) on even/odd TMEM lanes, so
+//            Re W[m] = D1[2m] - D2[2m+1], Im W[m] = D1[2m+1] + D2[2m]   (one lane-pair shuffle);
+//            the real row index IS the interleaved storage index of W.
+//   backward V = H^H W : A = H columns as a REAL (M x 2K) K-major matrix, B1 = W interleaved
+//            (2K x N), B2 = (-i W) interleaved: D1 = Re V, D2 = Im V directly.
+// 3xTF32: x = hi + lo with hi = tf32 truncation (what the MMA reads from an fp32 word) and
+// lo = x - hi (exact); D += A_hi B_hi + A_hi B_lo + A_lo B_hi (the lo*lo term is below FP32 rounding).
+// H_lo is computed once per shard; the epilogues write the lo / rotated copies the NEXT step
+// consumes, so every operand arrives by TMA.
+//
+// Roles (128 threads, 1 CTA per 128-row x 64-column tile): thread 0 issues TMA into a 3-stage
+// mbarrier ring, one elected lane of warp 1 issues the 6 tcgen05.mma per 8-deep k step into two
+// 64-column TMEM accumulators and commits each stage back to its `empty` barrier; all 4 warps run
+// the epilogue from TMEM (tcgen05.ld 32x32b, lane quadrant per warp).
+#pragma once
+#include <cstdint>
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace chase {
+
+struct C64Params {
+  int M, N, K;             // output rows (complex: fwd counts real rows 2*M_complex), cols, k (real MMA k)
+  float alpha, beta, gamma;
+  // shift source and beta/output in the step's formats (see cgemm_tc.cu)
+  const float* S0;          // fwd: Re X plane; bwd: X interleaved
+  const float* S1;          // fwd: Im X plane
+  int64_t lds;
+  int shift_lo, shift_hi;   // complex output rows carrying the shift
+  int64_t shift_off;
+  float* Y0;                // fwd: W interleaved (real rows); bwd: Re V plane
+  float* Y1;                // fwd: (-i W) interleaved;        bwd: Im V plane
+  float* Y0lo;              // lo copies (may be null)
+  float* Y1lo;
+  int64_t ldy;              // in floats (fwd: 2*p rows; bwd: q)
+  int beta_on;
+};
+
+namespace tc {
+constexpr int BMR = 128;   // real rows per tile (fwd: 64 complex rows; bwd: 128 complex rows)
+constexpr int BN = 64;
+constexpr int BK = 32;     // real k per stage (one 128-byte row of tf32)
+constexpr int STAGES = 3;
+constexpr uint32_t A_BYTES = BMR * BK * 4;            // 16 KB
+constexpr uint32_t B_BYTES = BK * BN * 4;             // 8 KB
+constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 4 * B_BYTES;   // A hi/lo + B1/B2 hi/lo = 64 KB
+constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+  d |= (uint64_t)(layout & 7) << 61;        // 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
+               ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(taddr));
+}
+
+__device__ __forceinline__ float tf32_lo(float x) {     // x - trunc_tf32(x), exact
+  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+}  // namespace tc
+
+// FWD = true: forward step (A MN-major from H, output W interleaved + rotated + lo copies)
+// FWD = false: backward step (A K-major from H's columns, output V planar + lo planes)
+template <bool FWD>
+__global__ void __launch_bounds__(128, 1)
+    c64_step_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tAlo,
+                    const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB1lo,
+                    const __grid_constant__ CUtensorMap tB2, const __grid_constant__ CUtensorMap tB2lo,
+                    C64Params p) {
+  using namespace tc;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[STAGES], empty[STAGES], done;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int m0 = (blockIdx.x / tiles_n) * BMR;     // real-row (fwd) / complex-row (bwd) tile origin
+  const int n0 = (blockIdx.x % tiles_n) * BN;
+  const int KT = (p.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(&done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tmem_base;
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    tma_prefetch_desc(&tA);
+    tma_prefetch_desc(&tB1);
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
+      unsigned char* st = sm + s * STAGE_BYTES;
+      mbar_arrive_expect_tx(full + s, STAGE_BYTES);
+      const int k0 = kt * BK;
+      if constexpr (FWD) {
+        // A MN-major: 4 boxes of 32 real rows x BK k -> [row-chunk][k][32 floats] (128B, 32B atoms)
+#pragma unroll
+        for (int c = 0; c < BMR / 32; ++c) {
+          tma_load_2d(st + c * (BK * 128), &tA, m0 + 32 * c, k0, full + s);
+          tma_load_2d(st + A_BYTES + c * (BK * 128), &tAlo, m0 + 32 * c, k0, full + s);
+        }
+      } else {
+        // A K-major: one box of BK real k x 128 rows -> [row][32 floats]
+        tma_load_2d(st, &tA, k0, m0, full + s);
+        tma_load_2d(st + A_BYTES, &tAlo, k0, m0, full + s);
+      }
+      unsigned char* sb = st + 2 * A_BYTES;
+      tma_load_2d(sb, &tB1, k0, n0, full + s);
+      tma_load_2d(sb + B_BYTES, &tB1lo, k0, n0, full + s);
+      tma_load_2d(sb + 2 * B_BYTES, &tB2, k0, n0, full + s);
+      tma_load_2d(sb + 3 * B_BYTES, &tB2lo, k0, n0, full + s);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    uint32_t leader;
+    asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+    // instruction descriptor: F32 accumulate, TF32 A/B, A major (fwd MN / bwd K), B K-major, N, M = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((FWD ? 1u : 0u) << 15) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BMR >> 4) << 24);
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      mbar_wait(full + s, (kt / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (leader) {
+        const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+        const uint32_t sa = st, salo = st + A_BYTES, sb = st + 2 * A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          uint64_t da, dal;
+          if constexpr (FWD) {
+            da = sdesc(sa + kk * 1024, BK * 128, 512, 1);
+            dal = sdesc(salo + kk * 1024, BK * 128, 512, 1);
+          } else {
+            da = sdesc(sa + kk * 32, 16, 1024, 2);
+            dal = sdesc(salo + kk * 32, 16, 1024, 2);
+          }
+          const uint64_t db1 = sdesc(sb + kk * 32, 16, 1024, 2);
+          const uint64_t db1l = sdesc(sb + B_BYTES + kk * 32, 16, 1024, 2);
+          const uint64_t db2 = sdesc(sb + 2 * B_BYTES + kk * 32, 16, 1024, 2);
+          const uint64_t db2l = sdesc(sb + 3 * B_BYTES + kk * 32, 16, 1024, 2);
+          const uint32_t acc = (kt > 0 || kk > 0) ? 1u : 0u;
+          tc::mma_tf32(tm, da, db1, idesc, acc);            // D1 = A_hi B1_hi
+          tc::mma_tf32(tm, da, db1l, idesc, 1u);            //    + A_hi B1_lo
+          tc::mma_tf32(tm, dal, db1, idesc, 1u);            //    + A_lo B1_hi
+          tc::mma_tf32(tm + BN, da, db2, idesc, acc);       // D2 = A_hi B2_hi
+          tc::mma_tf32(tm + BN, da, db2l, idesc, 1u);
+          tc::mma_tf32(tm + BN, dal, db2, idesc, 1u);
+        }
+        tc::commit(empty + s);                              // smem slot free once these MMAs retire
+        if (kt == KT - 1) tc::commit(&done);
+      }
+      __syncwarp();
+    }
+  }
+  // ------------------------------------------------------------------ epilogue (all 4 warps)
+  mbar_wait(&done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const int row = m0 + 32 * warp + lane;          // real row (fwd) / complex row (bwd)
+  const uint32_t lane_base = tm + ((uint32_t)(32 * warp) << 16);
+  const float ag = p.alpha * p.gamma;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t r1[16], r2[16];
+    tc::ld16(lane_base + c0, r1);
+    tc::ld16(lane_base + BN + c0, r2);
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int n = n0 + c0 + j;
+      const float d1 = __uint_as_float(r1[j]), d2 = __uint_as_float(r2[j]);
+      if constexpr (FWD) {
+        // even lane (real row 2m): Re W = D1[2m] - D2[2m+1]; odd lane: Im W = D1[2m+1] + D2[2m]
+        const float d2p = __shfl_xor_sync(0xffffffffu, d2, 1);
+        const bool odd = (row & 1);
+        float v = odd ? (d1 + d2p) : (d1 - d2p);
+        v *= p.alpha;
+        const int mc = row >> 1;                         // complex row
+        if (n < p.N && row < p.M) {
+          if (mc >= p.shift_lo && mc < p.shift_hi) {
+            const float* src = odd ? p.S1 : p.S0;        // planar Re / Im of X
+            v -= ag * src[(int64_t)mc + p.shift_off + (int64_t)n * p.lds];
+          }
+          float* y = p.Y0 + (int64_t)row + (int64_t)n * p.ldy;
+          if (p.beta_on) v += p.beta * *y;
+        }
+        // rotated copy -i W: (Im, -Re) -> even lane takes Im from its partner, odd lane -Re
+        const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
+        if (n < p.N && row < p.M) {
+          const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
+          p.Y0[o] = v;
+          const float rot = odd ? -vp : vp;
+          if (p.Y1) p.Y1[o] = rot;
+          if (p.Y0lo) p.Y0lo[o] = tc::tf32_lo(v);
+          if (p.Y1lo) p.Y1lo[o] = tc::tf32_lo(rot);
+        }
+      } else {
+        if (n < p.N && row < p.M) {
+          float vr = p.alpha * d1, vi = p.alpha * d2;
+          if (row >= p.shift_lo && row < p.shift_hi) {
+            const float* src = p.S0 + 2 * ((int64_t)row + p.shift_off) + 2 * (int64_t)n * p.lds;   // interleaved X
+            vr -= ag * src[0];
+            vi -= ag * src[1];
+          }
+          const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
+          if (p.beta_on) {
+            vr += p.beta * p.Y0[o];
+            vi += p.beta * p.Y1[o];
+          }
+          p.Y0[o] = vr;
+          p.Y1[o] = vi;
+          if (p.Y0lo) p.Y0lo[o] = tc::tf32_lo(vr);
+          if (p.Y1lo) p.Y1lo[o] = tc::tf32_lo(vi);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(2 * BN));
+}
+
+}  // namespace chase

@@ -305,7 +305,8 @@ chase_status chase_init(chase_handle** out, const chase_init_args* a) {
   *out = nullptr;
   chase_handle* h = new chase_handle();
   try {
-    if (a->dtype != CHASE_C128 && a->dtype != CHASE_R64) throw UsageError("dtype must be CHASE_C128 or CHASE_R64");
+    if (a->dtype != CHASE_C128 && a->dtype != CHASE_R64 && a->dtype != CHASE_C64)
+      throw UsageError("dtype must be CHASE_C128, CHASE_C64 or CHASE_R64");
     h->dtype = a->dtype;
     if (a->N <= 0 || a->nev_max <= 0 || a->nex_max <= 0 || a->nev_max + (int64_t)a->nex_max > a->N)
       throw UsageError("invalid N / nev_max / nex_max");
@@ -418,7 +419,10 @@ chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H, int64_
     if (!H || !X || !Y || ncols < 0 || ldh < p) throw UsageError("bad pointers / sizes");
     if (ldx < (dir == 0 ? q : p) || ldy < (dir == 0 ? p : q)) throw UsageError("bad leading dimension");
     order_after_user(h);
-    hemm_step(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma);
+    if (h->c64())
+      c64_hemm_step(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma);
+    else
+      hemm_step(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma);
     CHASE_CUDA(cudaStreamSynchronize(h->stream));
     return CHASE_OK;
   });
@@ -432,7 +436,8 @@ chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, 
     if (!H || !V || !W || ncols < 0 || (ncols > 0 && !degrees)) throw UsageError("bad pointers");
     if (ldh < p || ldv < q || ldw < p) throw UsageError("bad leading dimension");
     order_after_user(h);
-    const int64_t mv = filter(h, H, ldh, V, ldv, W, ldw, ncols, degrees, b_sup, mu_1, mu_ne);
+    const int64_t mv = h->c64() ? c64_filter(h, H, ldh, V, ldv, ncols, degrees, b_sup, mu_1, mu_ne)
+                                : filter(h, H, ldh, V, ldv, W, ldw, ncols, degrees, b_sup, mu_1, mu_ne);
     CHASE_CUDA(cudaStreamSynchronize(h->stream));
     if (matvecs) *matvecs = mv;
     return CHASE_OK;
@@ -443,6 +448,7 @@ chase_status chase_lanczos(chase_handle* h, const void* H, int64_t ldh, int32_t 
                            double* mu_1, double* mu_ne, double* nu) {
   return guarded(h, [&]() {
     if (!H || ldh < h->grid.rows.len || n_e <= 0 || n_e > h->grid.N) throw UsageError("bad arguments");
+    if (h->c64()) throw UsageError("chase_lanczos: CHASE_C64 is not implemented yet (filter / hemm_step only)");
     order_after_user(h);
     LanczosOut o = lanczos(h, H, ldh, n_e);
     if (b_sup) *b_sup = o.b_sup;
@@ -469,6 +475,7 @@ chase_status chase_solve(chase_handle* h, const void* H, int64_t ldh, int64_t N,
                          void* ritz_vectors, int64_t ldv, chase_report* report) {
   return guarded(h, [&]() {
     if (N != h->grid.N) throw UsageError("N differs from chase_init");
+    if (h->c64()) throw UsageError("chase_solve: CHASE_C64 is not implemented yet (filter / hemm_step only)");
     if (!(nev > 0 && nex > 0 && (int64_t)nev + nex <= N && tol > 0 && deg >= 1))
       throw UsageError("invalid nev / nex / tol / deg (S:407)");
     if (nev + nex > h->n_e_max) throw UsageError("nev + nex exceeds nev_max + nex_max of chase_init");
@@ -495,7 +502,7 @@ chase_status chase_finalize(chase_handle* h) {
   if (!h) return CHASE_E_USAGE;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz})
+  for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo})
     b->release();
   if (h->rowc) ncclCommDestroy(h->rowc);
   if (h->colc) ncclCommDestroy(h->colc);

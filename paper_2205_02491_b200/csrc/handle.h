@@ -67,7 +67,8 @@ struct chase_handle {
   chase::Grid grid;
   int dtype = CHASE_C128;              // CHASE_C128 (complex Hermitian) or CHASE_R64 (real symmetric)
   bool real() const { return dtype == CHASE_R64; }
-  size_t es() const { return real() ? 8 : 16; }          // bytes per element
+  bool c64() const { return dtype == CHASE_C64; }
+  size_t es() const { return dtype == CHASE_C128 ? 16 : 8; }   // bytes per element
   int nd() const { return real() ? 1 : 2; }              // doubles per element
   int device = 0;
   int world_size = 1;
@@ -78,6 +79,9 @@ struct chase_handle {
   int n_e_max = 0;
   // workspace
   chase::DBuf V, W, HV, V2, G, G2, Z, scratch, red, lz;
+  chase::DBuf Hlo;                     // c64: 3xTF32 lo part of the caller's H shard
+  const void* hlo_src = nullptr;
+  int64_t hlo_ld = 0;
   std::vector<double> host_scratch;
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -110,6 +114,13 @@ LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e);
 
 void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
                   int ncols, uint64_t seed, uint32_t stream_id);
+
+// complex-single (c64) path: tcgen05 3xTF32 fused step and filter (c64.cu)
+void allreduce_c64(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows, int64_t ld, int ncols);
+void c64_hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx, void* Y,
+                   int64_t ldy, int ncols, double alpha, double beta, double gamma);
+int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, int ncols, const int* degrees,
+                   double b_sup, double mu_1, double mu_ne);
 
 chase_status solve(chase_handle* h, const void* H, int64_t ldh, int nev, int nex, int deg,
                    double tol, double* ritz_values, void* ritz_vectors, int64_t ldv,

@@ -8,17 +8,19 @@ from chase_gen import make_matrix
 from chase_gen.device import DeviceG2
 
 real = len(sys.argv) > 3 and sys.argv[3] == "r64"
+single = len(sys.argv) > 3 and sys.argv[3] == "c64"
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 30000
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 3000
 from chase_gen.device import device_matrix
-dt = torch.float64 if real else torch.complex128
+dt = torch.float64 if real else (torch.complex64 if single else torch.complex128)
 M = make_matrix("uniform", N, "r2" if real else "g2", seed=1)
-H = torch.empty((N, N), dtype=dt, device="cuda").t()
+H = torch.empty((N, N), dtype=torch.float64 if real else torch.complex128, device="cuda").t()
 device_matrix(M).fill(H, 0, 0)
+H = H.to(dt)
 V = torch.randn((n, N), dtype=dt, device="cuda").t()
 W = torch.zeros((n, N), dtype=dt, device="cuda").t()
-ch = pkg.Chase(N, n - 10, 10, dtype="r64" if real else "c128")
-if not real:
+ch = pkg.Chase(N, n - 10, 10, dtype="r64" if real else ("c64" if single else "c128"))
+if not real and not single:
     ch.set_option("gemm3m", 1 if (len(sys.argv) <= 3 or sys.argv[3] == "3m") else 0)
 for d in (0, 1):
     ch.hemm_step(d, H, V if d == 0 else W, W if d == 0 else V, n, 1e-3, 0.5, 0.3)
