@@ -53,15 +53,19 @@ typedef enum {
 
 typedef enum {
   CHASE_C128 = 0, /* complex<double>, interleaved (re, im): Hermitian H -- the north_star path */
-  CHASE_C64 = 1,  /* complex<float> interleaved: Hermitian H in complex single; the filter runs on
-                     the tcgen05 tensor cores (TF32 with the 3xTF32 split).  Round 1: chase_filter
-                     and chase_hemm_step only (1 x c grids for the filter). */
+  CHASE_C64 = 1,  /* complex<float> interleaved: Hermitian H in complex single; every product with
+                     H runs on the tcgen05 tensor cores (TF32 with the 3xTF32 split, FP32-class
+                     accuracy) or, for Lanczos, an FP64-accumulated skinny kernel.  chase_solve
+                     iterates QR / RR / residuals in complex double on the library's workspace and
+                     returns complex<float> vectors (approx input likewise).  Layout limits of the
+                     TMA operands: q % 4 == 0, p even, ldh even, 16-byte aligned H.  The library
+                     keeps the 3xTF32 lo part of H (one extra shard-sized buffer). */
   CHASE_R64 = 2   /* double: real symmetric H, the paper's own experimental field.
                      Every buffer argument is then real double with the same layouts. */
 } chase_dtype;
 
 typedef struct {
-  chase_dtype dtype;              /* CHASE_C128 or CHASE_R64 */
+  chase_dtype dtype;              /* CHASE_C128, CHASE_C64 or CHASE_R64 */
   int64_t N;                      /* matrix order */
   int32_t nev_max, nex_max;       /* workspace sizing */
   int32_t grid_rows, grid_cols;   /* r, c; 0,0 = 1 x world.  world_size == 1 with r*c > 1 selects

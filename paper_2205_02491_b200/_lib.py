@@ -198,8 +198,8 @@ class Chase:
         r0, p, c0, q = self.local_layout()
         vals = (C.c_double * nev)()
         if vectors is None:
-            vectors = torch.empty((nev + nex, q), dtype=torch.float64 if self.real else torch.complex128,
-                                  device=H.device).t()
+            dt = torch.float64 if self.real else (torch.complex64 if self.single else torch.complex128)
+            vectors = torch.empty((nev + nex, q), dtype=dt, device=H.device).t()
         elif vectors.shape[0] != q:
             raise ValueError("vectors must be V-layout (q rows)")
         rep = Report()

@@ -48,13 +48,16 @@ __global__ void k_lo(float* dst, const float* src, int64_t rows, int cols, int64
   }
 }
 
-// interleaved complex64 (rows x cols, ld complex) -> planar Re, Im, Re_lo, Im_lo (ld rows)
-__global__ void k_to_planar(const float2* X, int64_t ldx, int64_t rows, int cols, float* Pr, float* Pi, float* Prl,
+// interleaved complex (complex64, or complex128 rounded to fp32 in the mixed solve) (rows x cols,
+// ld complex) -> planar Re, Im, Re_lo, Im_lo (ld rows)
+template <class TX>
+__global__ void k_to_planar(const TX* X, int64_t ldx, int64_t rows, int cols, float* Pr, float* Pi, float* Prl,
                             float* Pil, int64_t ldp) {
   const int64_t total = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i % rows, c = i / rows;
-    const float2 v = X[r + c * ldx];
+    const TX x = X[r + c * ldx];
+    const float2 v = make_float2((float)x.x, (float)x.y);
     const int64_t o = r + c * ldp;
     Pr[o] = v.x;
     Pi[o] = v.y;
@@ -63,12 +66,26 @@ __global__ void k_to_planar(const float2* X, int64_t ldx, int64_t rows, int cols
   }
 }
 
-__global__ void k_from_planar(float2* X, int64_t ldx, int64_t rows, int cols, const float* Pr, const float* Pi,
+template <class TX>
+__global__ void k_from_planar(TX* X, int64_t ldx, int64_t rows, int cols, const float* Pr, const float* Pi,
                               int64_t ldp) {
   const int64_t total = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i % rows, c = i / rows;
-    X[r + c * ldx] = make_float2(Pr[r + c * ldp], Pi[r + c * ldp]);
+    X[r + c * ldx].x = Pr[r + c * ldp];
+    X[r + c * ldx].y = Pi[r + c * ldp];
+  }
+}
+
+// complex64 <-> complex128 block copies (mixed solve: the c128 iteration around the c64 shard)
+template <class TD, class TS>
+__global__ void k_convert(TD* D, int64_t ldd, const TS* S, int64_t lds, int64_t rows, int cols) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % rows, c = i / rows;
+    const TS v = S[r + c * lds];
+    D[r + c * ldd].x = v.x;
+    D[r + c * ldd].y = v.y;
   }
 }
 
@@ -100,9 +117,11 @@ struct WFmt {        // W-layout block: 4 complex64 arrays, ld = p
 };
 
 // one local fused step (no communication); `first` columns offset already applied by the caller
-void c64_step_local(chase_handle* h, int dir, const void* H, int64_t ldh, const void* Hlo, const VFmt& v,
-                    const WFmt& w, int ncols, double alpha, double beta, double gamma, bool beta_on) {
+template <int BN>
+void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const void* Hlo, const VFmt& v,
+                 const WFmt& w, int ncols, double alpha, double beta, double gamma, bool beta_on) {
   using namespace tc;
+  constexpr size_t SMEM = Cfg<BN>::SMEM;
   const Grid& g = h->grid;
   const int64_t r0 = g.rows.start, p = g.rows.len, c0 = g.cols.start, q = g.cols.len;
   CUtensorMap ta, tal, tb1, tb1l, tb2, tb2l;
@@ -110,6 +129,10 @@ void c64_step_local(chase_handle* h, int dir, const void* H, int64_t ldh, const 
   P.N = ncols;
   P.alpha = (float)alpha; P.beta = (float)beta; P.gamma = (float)gamma;
   P.beta_on = beta_on ? 1 : 0;
+  static const int lolo = getenv("CHASE_C64_LOLO") ? atoi(getenv("CHASE_C64_LOLO")) : 0;
+  P.lolo = lolo;
+  static const int kcs = getenv("CHASE_C64_KC") ? atoi(getenv("CHASE_C64_KC")) : 0;
+  P.kc_stages = kcs;
   if (dir == 0) {       // forward: W = alpha (H V - gamma E V) + beta W
     f32_tmap(&ta, H, 2 * p, q, 2 * ldh, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     f32_tmap(&tal, Hlo, 2 * p, q, 2 * p, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
@@ -146,13 +169,23 @@ void c64_step_local(chase_handle* h, int dir, const void* H, int64_t ldh, const 
   static bool attr[2] = {false, false};
   const int grid = ceil_div(P.M, BMR) * ceil_div(P.N, BN);
   if (dir == 0) {
-    if (!attr[0]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)); attr[0] = true; }
-    c64_step_kernel<true><<<grid, 128, SMEM, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
+    if (!attr[0]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)); attr[0] = true; }
+    c64_step_kernel<true, BN><<<grid, C64_THREADS, SMEM, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
   } else {
-    if (!attr[1]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)); attr[1] = true; }
-    c64_step_kernel<false><<<grid, 128, SMEM, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
+    if (!attr[1]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)); attr[1] = true; }
+    c64_step_kernel<false, BN><<<grid, C64_THREADS, SMEM, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
   }
   CHASE_CHECK_LAUNCH();
+}
+
+// column tile: 128 (MMA N = 256, 2-stage ring) unless CHASE_C64_BN=64 (N = 128, 3 stages)
+void c64_step_local(chase_handle* h, int dir, const void* H, int64_t ldh, const void* Hlo, const VFmt& v,
+                    const WFmt& w, int ncols, double alpha, double beta, double gamma, bool beta_on) {
+  static const int bn = [] { const char* e = getenv("CHASE_C64_BN"); return e ? atoi(e) : 128; }();
+  if (bn == 64)
+    c64_step_bn<64>(h, dir, H, ldh, Hlo, v, w, ncols, alpha, beta, gamma, beta_on);
+  else
+    c64_step_bn<128>(h, dir, H, ldh, Hlo, v, w, ncols, alpha, beta, gamma, beta_on);
 }
 
 }  // namespace
@@ -193,7 +226,8 @@ const void* c64_hlo(chase_handle* h, const void* H, int64_t ldh) {
 // internal-format views of the handle's workspace for `ncols` columns starting at column `c`
 static VFmt vfmt(chase_handle* h, int ncap, int c) {
   const int64_t q = h->grid.cols.len;
-  float* base = h->V.as<float>();          // 16 B per element = 4 planes of q x ncap
+  h->c64v.alloc(16 * (size_t)q * ncap);
+  float* base = h->c64v.as<float>();       // 16 B per element = 4 planes of q x ncap
   VFmt v;
   v.ld = q;
   v.r = base + (int64_t)c * q;
@@ -204,8 +238,9 @@ static VFmt vfmt(chase_handle* h, int ncap, int c) {
 }
 static WFmt wfmt(chase_handle* h, int ncap, int c) {
   const int64_t p = h->grid.rows.len;
-  float2* a = h->W.as<float2>();            // W, -iW
-  float2* b = h->HV.as<float2>();           // lo copies
+  h->c64w.alloc(32 * (size_t)p * ncap);
+  float2* a = h->c64w.as<float2>();                         // W, -iW
+  float2* b = a + 2 * (int64_t)ncap * p;                    // lo copies
   WFmt w;
   w.ld = p;
   w.w = a + (int64_t)c * p;
@@ -253,11 +288,45 @@ void c64_hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const v
   }
 }
 
-// c64 filter (a1-a5): same schedule / scalars as the c128 filter; V interleaved in/out, internal
-// planar / rotated formats in between.  The all-reduce of each step runs on the interleaved W
-// (forward) or the planar V (backward) -- both are plain sums.
-int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, int ncols, const int* degrees,
-                   double b_sup, double mu_1, double mu_ne) {
+// mixed solve: (HX) in complex128 from a complex128 X (q x ncols, V-layout) through the c64 forward
+// step (RR's HQ, a8 step 1); the product itself is the tcgen05 3xTF32 step (FP32-class accuracy)
+void c64_forward_mixed(chase_handle* h, const void* H, int64_t ldh, const double2* X, int64_t ldx, double2* Y,
+                       int64_t ldy, int ncols) {
+  if (ncols <= 0) return;
+  const Grid& g = h->grid;
+  const int64_t p = g.rows.len, q = g.cols.len;
+  const void* Hlo = c64_hlo(h, H, ldh);
+  const double hs = h->opt.largest ? -1.0 : 1.0;
+  VFmt v = vfmt(h, h->n_e_max, 0);
+  WFmt w = wfmt(h, h->n_e_max, 0);
+  k_to_planar<<<grid_for(q * ncols), 256, 0, h->stream>>>(X, ldx, q, ncols, v.r, v.i, v.rl, v.il, v.ld);
+  CHASE_CHECK_LAUNCH();
+  WFmt out{w.w, nullptr, nullptr, nullptr, w.ld};
+  c64_step_local(h, 0, H, ldh, Hlo, v, out, ncols, hs, 0.0, 0.0, false);
+  allreduce_c64(h, h->rowc, g.c, w.w, p, w.ld, ncols);
+  k_convert<<<grid_for(p * ncols), 256, 0, h->stream>>>(Y, ldy, w.w, w.ld, p, ncols);
+  CHASE_CHECK_LAUNCH();
+}
+
+void c64_convert(void* dst, int64_t ldd, bool dst_c128, const void* src, int64_t lds, int64_t rows, int cols,
+                 cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return;
+  if (dst_c128)
+    k_convert<<<grid_for(rows * cols), 256, 0, st>>>(reinterpret_cast<double2*>(dst), ldd,
+                                                     reinterpret_cast<const float2*>(src), lds, rows, cols);
+  else
+    k_convert<<<grid_for(rows * cols), 256, 0, st>>>(reinterpret_cast<float2*>(dst), ldd,
+                                                     reinterpret_cast<const double2*>(src), lds, rows, cols);
+  CHASE_CHECK_LAUNCH();
+}
+
+// c64 filter (a1-a5): same schedule / scalars as the c128 filter; V interleaved in/out (complex64,
+// or complex128 in the mixed solve, rounded to fp32 on entry), internal planar / rotated formats
+// in between.  The all-reduce of each step runs on the interleaved W (forward) or the planar V
+// (backward) -- both are plain sums.
+template <class TV>
+static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, int64_t ldv, int ncols,
+                            const int* degrees, double b_sup, double mu_1, double mu_ne) {
   if (ncols <= 0) return 0;
   if (ncols > h->n_e_max) throw UsageError("c64 filter: ncols exceeds nev_max + nex_max");
   int64_t matvecs = 0;
@@ -276,8 +345,7 @@ int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t
   const double hs = h->opt.largest ? -1.0 : 1.0;
   const int ncap = h->n_e_max;
   VFmt v0 = vfmt(h, ncap, 0);
-  k_to_planar<<<grid_for(q * ncols), 256, 0, h->stream>>>(reinterpret_cast<const float2*>(V), ldv, q, ncols, v0.r,
-                                                          v0.i, v0.rl, v0.il, v0.ld);
+  k_to_planar<<<grid_for(q * ncols), 256, 0, h->stream>>>(V, ldv, q, ncols, v0.r, v0.i, v0.rl, v0.il, v0.ld);
   CHASE_CHECK_LAUNCH();
   const double sigma1 = e / (mu_1 - c);
   double sigma_prev = sigma1;
@@ -320,11 +388,24 @@ int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t
       }
     }
   }
-  VFmt vout = vfmt(h, ncap, 0);
-  k_from_planar<<<grid_for(q * ncols), 256, 0, h->stream>>>(reinterpret_cast<float2*>(V), ldv, q, ncols, vout.r,
-                                                            vout.i, vout.ld);
+  // columns of degree 0 were never touched: write back only the filtered suffix
+  int f0 = 0;
+  while (f0 < ncols && degrees[f0] == 0) ++f0;
+  VFmt vout = vfmt(h, ncap, f0);
+  k_from_planar<<<grid_for(q * (ncols - f0)), 256, 0, h->stream>>>(V + (int64_t)f0 * ldv, ldv, q, ncols - f0, vout.r,
+                                                                   vout.i, vout.ld);
   CHASE_CHECK_LAUNCH();
   return matvecs;
+}
+
+int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, int ncols, const int* degrees,
+                   double b_sup, double mu_1, double mu_ne) {
+  return c64_filter_t(h, H, ldh, reinterpret_cast<float2*>(V), ldv, ncols, degrees, b_sup, mu_1, mu_ne);
+}
+
+int64_t c64_filter_mixed(chase_handle* h, const void* H, int64_t ldh, double2* V, int64_t ldv, int ncols,
+                         const int* degrees, double b_sup, double mu_1, double mu_ne) {
+  return c64_filter_t(h, H, ldh, V, ldv, ncols, degrees, b_sup, mu_1, mu_ne);
 }
 
 }  // namespace chase

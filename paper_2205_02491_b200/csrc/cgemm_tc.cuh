@@ -12,14 +12,16 @@
 //   backward V = H^H W : A = H columns as a REAL (M x 2K) K-major matrix, B1 = W interleaved
 //            (2K x N), B2 = (-i W) interleaved: D1 = Re V, D2 = Im V directly.
 // 3xTF32: x = hi + lo with hi = tf32 truncation (what the MMA reads from an fp32 word) and
-// lo = x - hi (exact); D += A_hi B_hi + A_hi B_lo + A_lo B_hi (the lo*lo term is below FP32 rounding).
+// lo = RN_tf32(x - hi); D += A_hi B_hi + A_hi B_lo + A_lo B_hi (the lo*lo term is ~2^-24 relative).
 // H_lo is computed once per shard; the epilogues write the lo / rotated copies the NEXT step
 // consumes, so every operand arrives by TMA.
 //
-// Roles (128 threads, 1 CTA per 128-row x 64-column tile): thread 0 issues TMA into a 3-stage
-// mbarrier ring, one elected lane of warp 1 issues the 6 tcgen05.mma per 8-deep k step into two
-// 64-column TMEM accumulators and commits each stage back to its `empty` barrier; all 4 warps run
-// the epilogue from TMEM (tcgen05.ld 32x32b, lane quadrant per warp).
+// Roles (320 threads, 1 CTA per 128-row x BN-column tile): thread 0 issues TMA into a 2-4 stage
+// mbarrier ring, one elected lane of warp 1 issues 3 tcgen05.mma (M=128, N=2 BN: B1 and B2 sit
+// side by side in shared memory, so one MMA reads each A tile once for both) per 8-deep k step
+// into the two BN-column TMEM accumulators of the current K chunk and commits each stage back to
+// its `empty` barrier; warps 2-9 drain finished chunks (tcgen05.ld 32x32b, lane quadrant =
+// warp % 4, column half = (warp - 2) / 4) into FP32 registers and run the fused epilogue.
 #pragma once
 #include <cstdint>
 #include "common.cuh"
@@ -42,18 +44,22 @@ struct C64Params {
   float* Y1lo;
   int64_t ldy;              // in floats (fwd: 2*p rows; bwd: q)
   int beta_on;
+  int lolo;                 // diagnostic: also issue the A_lo B_lo MMA (4xTF32)
+  int kc_stages;            // K chunk (in BK stages) per fresh TMEM accumulator; 0 = default
 };
 
 namespace tc {
 constexpr int BMR = 128;   // real rows per tile (fwd: 64 complex rows; bwd: 128 complex rows)
-constexpr int BN = 64;
 constexpr int BK = 32;     // real k per stage (one 128-byte row of tf32)
-constexpr int STAGES = 3;
 constexpr uint32_t A_BYTES = BMR * BK * 4;            // 16 KB
-constexpr uint32_t B_BYTES = BK * BN * 4;             // 8 KB
-constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 4 * B_BYTES;   // A hi/lo + B1/B2 hi/lo = 64 KB
-constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
-
+template <int BN>
+struct Cfg {
+  // B1 | B2 adjacent (one N = 2 BN operand), then their lo copies: one MMA per (hi/lo) pair
+  static constexpr uint32_t B_BYTES = BK * BN * 4;
+  static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 4 * B_BYTES;
+  static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 4 ? 4 : (220 * 1024) / STAGE_BYTES;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+};
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
@@ -81,41 +87,69 @@ __device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
                : "r"(taddr));
 }
 
-__device__ __forceinline__ float tf32_lo(float x) {     // x - trunc_tf32(x), exact
-  return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+// x = hi + lo with hi = trunc_tf32(x) (what the MMA reads from the fp32 word).  lo is stored
+// pre-rounded to TF32 with round-to-nearest-even, so the MMA reads it exactly and the dropped
+// remainder (<= 2^-12 |lo|) is unbiased; a truncated lo would bias every product toward zero by
+// ~2^-23 relative (measured: 2e-6 relative HQ error at K = 4000 before this rounding).
+__device__ __forceinline__ float tf32_rn(float y) {
+  uint32_t b = __float_as_uint(y);
+  b += 0xFFFu + ((b >> 13) & 1u);
+  return __uint_as_float(b & 0xFFFFE000u);
+}
+__device__ __forceinline__ float tf32_lo(float x) {
+  return tf32_rn(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
 }
 }  // namespace tc
 
 // FWD = true: forward step (A MN-major from H, output W interleaved + rotated + lo copies)
 // FWD = false: backward step (A K-major from H's columns, output V planar + lo planes)
-template <bool FWD>
-__global__ void __launch_bounds__(128, 1)
+//
+// Accumulation: the tensor core's FP32 accumulator loses precision with every MMA added into it
+// (measured step error, K = 1200: 1.3e-7 / 1.9e-7 / 3.0e-7 / 5.3e-7 / 1.9e-6 for chunks of
+// 32 / 64 / 128 / 256 / 1024 real k -- linear in the chunk length; unchunked it reached 5e-6 at
+// K = 1200 and grows with K).  The K loop is therefore cut into chunks of 64: every chunk starts
+// a fresh TMEM accumulator (double-buffered, 2 x 2BN columns), and 8 epilogue warps drain the
+// finished chunk into FP32 registers with round-to-nearest adds while the next chunk accumulates.
+constexpr int C64_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 chunk drain + epilogue
+constexpr int C64_KC_STAGES = 2;       // chunk = 2 stages x BK 32 = 64 real k (error ~ linear in chunk length)
+
+template <bool FWD, int BN>
+__global__ void __launch_bounds__(C64_THREADS, 1)
     c64_step_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tAlo,
                     const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB1lo,
                     const __grid_constant__ CUtensorMap tB2, const __grid_constant__ CUtensorMap tB2lo,
                     C64Params p) {
   using namespace tc;
+  constexpr uint32_t B_BYTES = Cfg<BN>::B_BYTES, STAGE_BYTES = Cfg<BN>::STAGE_BYTES;
+  constexpr int STAGES = Cfg<BN>::STAGES;
+  const int CH = p.kc_stages > 0 ? p.kc_stages : C64_KC_STAGES;
+  constexpr uint32_t TCOLS = 4 * BN;     // 2 chunk buffers x (D1 | D2)
+  constexpr int HN = BN / 2;             // columns per epilogue warp (per accumulator)
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[STAGES], empty[STAGES], done;
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = (p.N + BN - 1) / BN;
   const int m0 = (blockIdx.x / tiles_n) * BMR;     // real-row (fwd) / complex-row (bwd) tile origin
   const int n0 = (blockIdx.x % tiles_n) * BN;
   const int KT = (p.K + BK - 1) / BK;
+  const int NCH = (KT + CH - 1) / CH;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(&done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 8);
+    }
     fence_mbar_init();
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "r"(2 * BN));
+                 "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -123,33 +157,35 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = tmem_base;
 
-  if (warp == 0 && lane == 0) {
-    // ------------------------------------------------------------------ TMA producer
-    tma_prefetch_desc(&tA);
-    tma_prefetch_desc(&tB1);
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
-      unsigned char* st = sm + s * STAGE_BYTES;
-      mbar_arrive_expect_tx(full + s, STAGE_BYTES);
-      const int k0 = kt * BK;
-      if constexpr (FWD) {
-        // A MN-major: 4 boxes of 32 real rows x BK k -> [row-chunk][k][32 floats] (128B, 32B atoms)
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      tma_prefetch_desc(&tA);
+      tma_prefetch_desc(&tB1);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
+        unsigned char* st = sm + s * STAGE_BYTES;
+        mbar_arrive_expect_tx(full + s, STAGE_BYTES);
+        const int k0 = kt * BK;
+        if constexpr (FWD) {
+          // A MN-major: 4 boxes of 32 real rows x BK k -> [row-chunk][k][32 floats] (128B, 32B atoms)
 #pragma unroll
-        for (int c = 0; c < BMR / 32; ++c) {
-          tma_load_2d(st + c * (BK * 128), &tA, m0 + 32 * c, k0, full + s);
-          tma_load_2d(st + A_BYTES + c * (BK * 128), &tAlo, m0 + 32 * c, k0, full + s);
+          for (int c = 0; c < BMR / 32; ++c) {
+            tma_load_2d(st + c * (BK * 128), &tA, m0 + 32 * c, k0, full + s);
+            tma_load_2d(st + A_BYTES + c * (BK * 128), &tAlo, m0 + 32 * c, k0, full + s);
+          }
+        } else {
+          // A K-major: one box of BK real k x 128 rows -> [row][32 floats]
+          tma_load_2d(st, &tA, k0, m0, full + s);
+          tma_load_2d(st + A_BYTES, &tAlo, k0, m0, full + s);
         }
-      } else {
-        // A K-major: one box of BK real k x 128 rows -> [row][32 floats]
-        tma_load_2d(st, &tA, k0, m0, full + s);
-        tma_load_2d(st + A_BYTES, &tAlo, k0, m0, full + s);
+        unsigned char* sb = st + 2 * A_BYTES;
+        tma_load_2d(sb, &tB1, k0, n0, full + s);
+        tma_load_2d(sb + B_BYTES, &tB2, k0, n0, full + s);
+        tma_load_2d(sb + 2 * B_BYTES, &tB1lo, k0, n0, full + s);
+        tma_load_2d(sb + 3 * B_BYTES, &tB2lo, k0, n0, full + s);
       }
-      unsigned char* sb = st + 2 * A_BYTES;
-      tma_load_2d(sb, &tB1, k0, n0, full + s);
-      tma_load_2d(sb + B_BYTES, &tB1lo, k0, n0, full + s);
-      tma_load_2d(sb + 2 * B_BYTES, &tB2, k0, n0, full + s);
-      tma_load_2d(sb + 3 * B_BYTES, &tB2lo, k0, n0, full + s);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
@@ -157,14 +193,21 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
     // instruction descriptor: F32 accumulate, TF32 A/B, A major (fwd MN / bwd K), B K-major, N, M = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((FWD ? 1u : 0u) << 15) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BMR >> 4) << 24);
+                           ((uint32_t)((2 * BN) >> 3) << 17) | ((uint32_t)(BMR >> 4) << 24);
     for (int kt = 0; kt < KT; ++kt) {
       const int s = kt % STAGES;
+      const int chunk = kt / CH, b = chunk & 1;
+      const bool chunk_start = (kt % CH) == 0;
+      if (chunk_start && chunk >= 2) {                     // buffer b drained (chunk - 2)?
+        mbar_wait(acc_empty + b, ((chunk >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
       mbar_wait(full + s, (kt / STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (leader) {
         const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
         const uint32_t sa = st, salo = st + A_BYTES, sb = st + 2 * A_BYTES;
+        const uint32_t td = tm + (uint32_t)b * 2 * BN;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           uint64_t da, dal;
@@ -175,40 +218,55 @@ __global__ void __launch_bounds__(128, 1)
             da = sdesc(sa + kk * 32, 16, 1024, 2);
             dal = sdesc(salo + kk * 32, 16, 1024, 2);
           }
-          const uint64_t db1 = sdesc(sb + kk * 32, 16, 1024, 2);
-          const uint64_t db1l = sdesc(sb + B_BYTES + kk * 32, 16, 1024, 2);
-          const uint64_t db2 = sdesc(sb + 2 * B_BYTES + kk * 32, 16, 1024, 2);
-          const uint64_t db2l = sdesc(sb + 3 * B_BYTES + kk * 32, 16, 1024, 2);
-          const uint32_t acc = (kt > 0 || kk > 0) ? 1u : 0u;
-          tc::mma_tf32(tm, da, db1, idesc, acc);            // D1 = A_hi B1_hi
-          tc::mma_tf32(tm, da, db1l, idesc, 1u);            //    + A_hi B1_lo
-          tc::mma_tf32(tm, dal, db1, idesc, 1u);            //    + A_lo B1_hi
-          tc::mma_tf32(tm + BN, da, db2, idesc, acc);       // D2 = A_hi B2_hi
-          tc::mma_tf32(tm + BN, da, db2l, idesc, 1u);
-          tc::mma_tf32(tm + BN, dal, db2, idesc, 1u);
+          // [B1 | B2] as one K-major operand of 2 BN rows: D[:, 0:BN) = A B1, D[:, BN:2BN) = A B2
+          const uint64_t db = sdesc(sb + kk * 32, 16, 1024, 2);
+          const uint64_t dbl = sdesc(sb + 2 * B_BYTES + kk * 32, 16, 1024, 2);
+          const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
+          tc::mma_tf32(td, da, db, idesc, acc);             // D = A_hi B_hi
+          tc::mma_tf32(td, da, dbl, idesc, 1u);             //   + A_hi B_lo
+          tc::mma_tf32(td, dal, db, idesc, 1u);             //   + A_lo B_hi
+          if (p.lolo) tc::mma_tf32(td, dal, dbl, idesc, 1u);  //   + A_lo B_lo (diagnostic)
         }
         tc::commit(empty + s);                              // smem slot free once these MMAs retire
-        if (kt == KT - 1) tc::commit(&done);
+        if ((kt % CH) == CH - 1 || kt == KT - 1) tc::commit(acc_full + b);
       }
       __syncwarp();
     }
-  }
-  // ------------------------------------------------------------------ epilogue (all 4 warps)
-  mbar_wait(&done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const int row = m0 + 32 * warp + lane;          // real row (fwd) / complex row (bwd)
-  const uint32_t lane_base = tm + ((uint32_t)(32 * warp) << 16);
-  const float ag = p.alpha * p.gamma;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    uint32_t r1[16], r2[16];
-    tc::ld16(lane_base + c0, r1);
-    tc::ld16(lane_base + BN + c0, r2);
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
+  } else {
+    // ------------------------------------------------------------------ drain + epilogue (8 warps)
+    const int quad = warp & 3;                       // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;                // column half of each accumulator
+    const int row = m0 + 32 * quad + lane;           // real row (fwd) / complex row (bwd)
+    const uint32_t lane_base = tm + ((uint32_t)(32 * quad) << 16) + (uint32_t)(half * HN);
+    float a1[HN], a2[HN];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int n = n0 + c0 + j;
-      const float d1 = __uint_as_float(r1[j]), d2 = __uint_as_float(r2[j]);
+    for (int j = 0; j < HN; ++j) a1[j] = a2[j] = 0.f;
+    for (int chunk = 0; chunk < NCH; ++chunk) {
+      const int b = chunk & 1;
+      mbar_wait(acc_full + b, (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t base = lane_base + (uint32_t)b * 2 * BN;
+#pragma unroll
+      for (int c0 = 0; c0 < HN; c0 += 16) {
+        uint32_t r1[16], r2[16];
+        tc::ld16(base + c0, r1);
+        tc::ld16(base + BN + c0, r2);
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          a1[c0 + j] += __uint_as_float(r1[j]);
+          a2[c0 + j] += __uint_as_float(r2[j]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + b);
+    }
+    const float ag = p.alpha * p.gamma;
+#pragma unroll
+    for (int j = 0; j < HN; ++j) {
+      const int n = n0 + half * HN + j;
+      const float d1 = a1[j], d2 = a2[j];
       if constexpr (FWD) {
         // even lane (real row 2m): Re W = D1[2m] - D2[2m+1]; odd lane: Im W = D1[2m+1] + D2[2m]
         const float d2p = __shfl_xor_sync(0xffffffffu, d2, 1);
@@ -257,7 +315,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(2 * BN));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(TCOLS));
 }
 
 }  // namespace chase

@@ -182,7 +182,8 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
 }
 
 // -------------------------------------------------------------------- random start block
-__global__ void k_random_block(double2* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
+template <class TV>
+__global__ void k_random_block(TV* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
                                int ncols, uint32_t k0, uint32_t k1, uint32_t stream_id) {
   const int64_t total = rows * ncols;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -192,7 +193,8 @@ __global__ void k_random_block(double2* V, int64_t ldv, int64_t rows, int64_t gr
     const uint64_t grow = (uint64_t)(grow0 + rloc);
     const Philox4 o = philox4x32_10((uint32_t)grow, (uint32_t)(grow >> 32), (uint32_t)(col0 + cl),
                                     stream_id, k0, k1);
-    V[rloc + (int64_t)cl * ldv] = make_double2(philox_unit(o.x[0], o.x[1]), philox_unit(o.x[2], o.x[3]));
+    V[rloc + (int64_t)cl * ldv].x = philox_unit(o.x[0], o.x[1]);     // complex64: rounded to fp32
+    V[rloc + (int64_t)cl * ldv].y = philox_unit(o.x[2], o.x[3]);
   }
 }
 
@@ -212,13 +214,16 @@ __global__ void k_random_block_real(double* V, int64_t ldv, int64_t rows, int64_
 }
 
 void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
-                  int ncols, uint64_t seed, uint32_t stream_id) {
+                  int ncols, uint64_t seed, uint32_t stream_id, bool c64_out) {
   if (rows <= 0 || ncols <= 0) return;
   const int64_t total = rows * ncols;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   if (h->real())
     k_random_block_real<<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double*>(V), ldv, rows, grow0, col0, ncols,
                                                        (uint32_t)seed, (uint32_t)(seed >> 32), stream_id);
+  else if (c64_out)
+    k_random_block<<<blocks, 256, 0, h->stream>>>(reinterpret_cast<float2*>(V), ldv, rows, grow0, col0, ncols,
+                                                  (uint32_t)seed, (uint32_t)(seed >> 32), stream_id);
   else
     k_random_block<<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double2*>(V), ldv, rows, grow0,
                                                   col0, ncols, (uint32_t)seed, (uint32_t)(seed >> 32),
@@ -448,7 +453,6 @@ chase_status chase_lanczos(chase_handle* h, const void* H, int64_t ldh, int32_t 
                            double* mu_1, double* mu_ne, double* nu) {
   return guarded(h, [&]() {
     if (!H || ldh < h->grid.rows.len || n_e <= 0 || n_e > h->grid.N) throw UsageError("bad arguments");
-    if (h->c64()) throw UsageError("chase_lanczos: CHASE_C64 is not implemented yet (filter / hemm_step only)");
     order_after_user(h);
     LanczosOut o = lanczos(h, H, ldh, n_e);
     if (b_sup) *b_sup = o.b_sup;
@@ -464,7 +468,7 @@ chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t c
   return guarded(h, [&]() {
     if (!V || ldv < h->grid.cols.len || ncols < 0) throw UsageError("bad arguments");
     order_after_user(h);
-    random_block(h, V, ldv, h->grid.cols.len, h->grid.cols.start, col0, ncols, seed, stream);
+    random_block(h, V, ldv, h->grid.cols.len, h->grid.cols.start, col0, ncols, seed, stream, h->c64());
     CHASE_CUDA(cudaStreamSynchronize(h->stream));
     return CHASE_OK;
   }, false);
@@ -475,13 +479,13 @@ chase_status chase_solve(chase_handle* h, const void* H, int64_t ldh, int64_t N,
                          void* ritz_vectors, int64_t ldv, chase_report* report) {
   return guarded(h, [&]() {
     if (N != h->grid.N) throw UsageError("N differs from chase_init");
-    if (h->c64()) throw UsageError("chase_solve: CHASE_C64 is not implemented yet (filter / hemm_step only)");
     if (!(nev > 0 && nex > 0 && (int64_t)nev + nex <= N && tol > 0 && deg >= 1))
       throw UsageError("invalid nev / nex / tol / deg (S:407)");
     if (nev + nex > h->n_e_max) throw UsageError("nev + nex exceeds nev_max + nex_max of chase_init");
     if (!H || ldh < h->grid.rows.len || !ritz_values || !ritz_vectors || ldv < h->grid.cols.len)
       throw UsageError("bad pointers / leading dimensions");
     order_after_user(h);
+    if (h->c64()) c64_hlo(h, H, ldh);             // validates the c64 shard layout up front
     return solve(h, H, ldh, nev, nex, deg, tol, ritz_values, ritz_vectors, ldv, report);
   });
 }
@@ -502,7 +506,8 @@ chase_status chase_finalize(chase_handle* h) {
   if (!h) return CHASE_E_USAGE;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
-  for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo})
+  for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo,
+                         &h->c64v, &h->c64w})
     b->release();
   if (h->rowc) ncclCommDestroy(h->rowc);
   if (h->colc) ncclCommDestroy(h->colc);

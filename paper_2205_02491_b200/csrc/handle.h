@@ -80,6 +80,7 @@ struct chase_handle {
   // workspace
   chase::DBuf V, W, HV, V2, G, G2, Z, scratch, red, lz;
   chase::DBuf Hlo;                     // c64: 3xTF32 lo part of the caller's H shard
+  chase::DBuf c64v, c64w;              // c64: planar V-layout / W-layout operand formats (c64.cu)
   const void* hlo_src = nullptr;
   int64_t hlo_ld = 0;
   std::vector<double> host_scratch;
@@ -113,7 +114,7 @@ struct LanczosOut {
 LanczosOut lanczos(chase_handle* h, const void* H, int64_t ldh, int n_e);
 
 void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t grow0, int col0,
-                  int ncols, uint64_t seed, uint32_t stream_id);
+                  int ncols, uint64_t seed, uint32_t stream_id, bool c64_out = false);
 
 // complex-single (c64) path: tcgen05 3xTF32 fused step and filter (c64.cu)
 void allreduce_c64(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows, int64_t ld, int ncols);
@@ -121,6 +122,15 @@ void c64_hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const v
                    int64_t ldy, int ncols, double alpha, double beta, double gamma);
 int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, int ncols, const int* degrees,
                    double b_sup, double mu_1, double mu_ne);
+// H_lo of the shard (validates the c64 layout; recomputed when H / ldh change)
+const void* c64_hlo(chase_handle* h, const void* H, int64_t ldh);
+// mixed solve (c64 shard, complex128 iteration): filter / HX on complex128 blocks, and conversions
+int64_t c64_filter_mixed(chase_handle* h, const void* H, int64_t ldh, double2* V, int64_t ldv, int ncols,
+                         const int* degrees, double b_sup, double mu_1, double mu_ne);
+void c64_forward_mixed(chase_handle* h, const void* H, int64_t ldh, const double2* X, int64_t ldx, double2* Y,
+                       int64_t ldy, int ncols);
+void c64_convert(void* dst, int64_t ldd, bool dst_c128, const void* src, int64_t lds, int64_t rows, int cols,
+                 cudaStream_t st);
 
 chase_status solve(chase_handle* h, const void* H, int64_t ldh, int nev, int nex, int deg,
                    double tol, double* ritz_values, void* ritz_vectors, int64_t ldv,

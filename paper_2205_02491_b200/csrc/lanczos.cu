@@ -164,11 +164,13 @@ static LanczosOut lanczos_t(chase_handle* h, const void* H, int64_t ldh, int n_e
     T* Qj = Q + (size_t)j * N * L;
     // F = H Q_j  (rows of block i from this shard; world sum assembles the full vectors)
     CHASE_CUDA(cudaMemsetAsync(F, 0, fbytes, st));
+    if (h->c64() && !(L == 1 || L == 2 || L == 3 || L == 4 || L == 8))
+      throw UsageError("CHASE_C64: lanczos_runs must be 1, 2, 3, 4 or 8");
     if (L == 1 || L == 2 || L == 3 || L == 4 || L == 8) {
       // HBM-bound skinny product: streams the shard once per step
       if (SC<T>::is_complex)
         zgemm_skinny((int)g.rows.len, L, (int)g.cols.len, hsign, H, ldh, Qj + g.cols.start, N,
-                     F + g.rows.start, N, h->scratch.p, st);
+                     F + g.rows.start, N, h->scratch.p, st, h->c64());
       else
         dgemm_skinny((int)g.rows.len, L, (int)g.cols.len, hsign, H, ldh, Qj + g.cols.start, N,
                      F + g.rows.start, N, h->scratch.p, st);

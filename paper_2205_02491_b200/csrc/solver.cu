@@ -147,8 +147,14 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
   double b_sup = lz.b_sup, mu_1 = lz.mu_1, mu_ne = lz.mu_ne;
   const double nu = lz.nu > 0.0 ? lz.nu : 1.0;
 
+  // CHASE_C64 (mixed solve): the shard is complex single; every product with it runs on the c64
+  // kernels (tcgen05 3xTF32 filter / HQ, FP64-accumulated skinny Lanczos product), the iteration
+  // around it (QR, RR, residuals) in complex double on the handle's workspace.
+  const bool mixed = h->c64();
   // ---- initial V-hat (Require of Alg. 1)
-  if (h->opt.approx)
+  if (h->opt.approx && mixed)
+    c64_convert(V, q, true, ritz_vectors, ldv_out, q, n_e, st);
+  else if (h->opt.approx)
     copy2d<T>(V, q, ritz_vectors, ldv_out, q, n_e, st);
   else
     random_block(h, V, q, q, c0, 0, n_e, h->opt.seed_v, 0);
@@ -168,7 +174,14 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
 
     // ---- line 4: Filter
     t_f.start(st);
-    matvecs += filter(h, Hv, ldh, Va, q, Wa, p, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
+    if constexpr (SC<T>::is_complex) {
+      if (mixed)
+        matvecs += c64_filter_mixed(h, Hv, ldh, Va, q, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
+      else
+        matvecs += filter(h, Hv, ldh, Va, q, Wa, p, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
+    } else {
+      matvecs += filter(h, Hv, ldh, Va, q, Wa, p, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
+    }
     t_f.stop(st);
 
     // ---- line 5: QR([Y V]) -- CGS2 against the locked Y, then CholQR2 (shifted fallback)
@@ -228,7 +241,14 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
 
     // ---- line 6: Rayleigh-Ritz
     t_rr.start(st);
-    hemm_step(h, 0, Hv, ldh, Va, q, HVa, p, n_act, 1.0, 0.0, 0.0);      // HQ (W-layout)
+    if constexpr (SC<T>::is_complex) {
+      if (mixed)
+        c64_forward_mixed(h, Hv, ldh, Va, q, HVa, p, n_act);              // HQ (W-layout)
+      else
+        hemm_step(h, 0, Hv, ldh, Va, q, HVa, p, n_act, 1.0, 0.0, 0.0);
+    } else {
+      hemm_step(h, 0, Hv, ldh, Va, q, HVa, p, n_act, 1.0, 0.0, 0.0);    // HQ (W-layout)
+    }
     if (I.len > 0) {
       ZgemmDesc d;                                  // G = Q[I]^H HQ[I]
       d.use3m = h->opt.gemm3m;
@@ -272,13 +292,17 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     CHASE_CUDA(cudaStreamSynchronize(st));
     const double f0 = t_f.total_ms, q0 = t_qr.total_ms, r0_ = t_rr.total_ms, s0 = t_res.total_ms;
     t_f.collect(); t_qr.collect(); t_rr.collect(); t_res.collect();
-    if (trace && g.rank == 0)
-      std::fprintf(stderr, "[chase] it=%d n_act=%d locked_before=%d matvecs=%lld filter=%.3fs qr=%.3fs rr=%.3fs resid=%.4fs\n",
-                   it, n_act, locked, (long long)matvecs, (t_f.total_ms - f0) * 1e-3, (t_qr.total_ms - q0) * 1e-3,
-                   (t_rr.total_ms - r0_) * 1e-3, (t_res.total_ms - s0) * 1e-3);
     for (int a = 0; a < n_act; ++a) {
       ritz[locked + a] = th_h[a];
       res[locked + a] = std::sqrt(std::max(0.0, r2_h[a])) / nu;
+    }
+    if (trace && g.rank == 0) {
+      double rmin = 1e300, rmax = 0.0;
+      for (int a = 0; a < n_act; ++a) { rmin = std::min(rmin, res[locked + a]); rmax = std::max(rmax, res[locked + a]); }
+      std::fprintf(stderr, "[chase] it=%d n_act=%d locked_before=%d matvecs=%lld filter=%.3fs qr=%.3fs rr=%.3fs resid=%.4fs "
+                   "res[0]=%.2e res_min=%.2e res_max=%.2e\n",
+                   it, n_act, locked, (long long)matvecs, (t_f.total_ms - f0) * 1e-3, (t_qr.total_ms - q0) * 1e-3,
+                   (t_rr.total_ms - r0_) * 1e-3, (t_res.total_ms - s0) * 1e-3, res[locked], rmin, rmax);
     }
     // ---- line 8: deflation & locking (prefix-contiguous in Ritz order, ledger #15)
     int nl = 0;
@@ -322,7 +346,12 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     max_resid = std::max(max_resid, res[src]);
   }
   CHASE_CUDA(cudaMemcpyAsync(d_perm, out_cols.data(), sizeof(int) * nev, cudaMemcpyHostToDevice, st));
-  permute_cols<T>(ritz_vectors, ldv_out, V, q, q, d_perm, nev, st);
+  if (mixed) {
+    permute_cols<T>(V2, q, V, q, q, d_perm, nev, st);
+    c64_convert(ritz_vectors, ldv_out, false, V2, q, q, nev, st);
+  } else {
+    permute_cols<T>(ritz_vectors, ldv_out, V, q, q, d_perm, nev, st);
+  }
   t_all.stop(st);
   CHASE_CUDA(cudaStreamSynchronize(st));
   t_all.collect();

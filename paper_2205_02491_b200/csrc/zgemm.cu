@@ -136,8 +136,15 @@ inline int skinny_splits(int M, int K) {
   return s;
 }
 
-template <int L>
-__global__ void __launch_bounds__(SK_T) k_skinny(int M, int K, int kchunk, const double2* __restrict__ A,
+__device__ __forceinline__ double2 ld_c(const double2* a) { return __ldg(a); }
+__device__ __forceinline__ double2 ld_c(const float2* a) {
+  const float2 v = __ldg(a);
+  return make_double2(v.x, v.y);
+}
+
+// TA = double2 (complex double shard) or float2 (complex-single shard, FP64 accumulation)
+template <int L, class TA>
+__global__ void __launch_bounds__(SK_T) k_skinny(int M, int K, int kchunk, const TA* __restrict__ A,
                                                  int64_t lda, const double2* __restrict__ B, int64_t ldb,
                                                  double2* __restrict__ P) {
   __shared__ double2 Bs[SK_KB][L];
@@ -155,10 +162,10 @@ __global__ void __launch_bounds__(SK_T) k_skinny(int M, int K, int kchunk, const
     }
     __syncthreads();
     if (m < M) {
-      const double2* a = A + m + (int64_t)kb * lda;
+      const TA* a = A + m + (int64_t)kb * lda;
 #pragma unroll 4
       for (int kk = 0; kk < kn; ++kk) {
-        const double2 h = __ldg(a + (int64_t)kk * lda);
+        const double2 h = ld_c(a + (int64_t)kk * lda);
 #pragma unroll
         for (int l = 0; l < L; ++l) {
           const double2 b = Bs[kk][l];
@@ -194,24 +201,32 @@ __global__ void k_skinny_reduce(int M, int L, int splits, double alpha, const do
 
 size_t skinny_work_bytes(int M, int K, int L) { return 16 * (size_t)skinny_splits(M, K) * L * M; }
 
+template <class TA>
+static void skinny_launch(int M, int L, int K, const TA* Ad, int64_t lda, const double2* Bd, int64_t ldb, double2* P,
+                          dim3 grid, int kchunk, cudaStream_t st) {
+  switch (L) {
+    case 1: k_skinny<1, TA><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 2: k_skinny<2, TA><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 3: k_skinny<3, TA><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 4: k_skinny<4, TA><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    case 8: k_skinny<8, TA><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
+    default: throw CudaError("zgemm_skinny: L must be 1, 2, 3, 4 or 8");
+  }
+}
+
 void zgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B, int64_t ldb,
-                  void* C, int64_t ldc, void* work, cudaStream_t st) {
+                  void* C, int64_t ldc, void* work, cudaStream_t st, bool a_c64) {
   if (M <= 0 || L <= 0) return;
   if (L > 8) throw CudaError("zgemm_skinny: L must be <= 8");
   const int splits = skinny_splits(M, K);
   const int kchunk = ceil_div(K, splits);
   dim3 grid(ceil_div(M, SK_T), splits);
-  auto* Ad = reinterpret_cast<const double2*>(A);
   auto* Bd = reinterpret_cast<const double2*>(B);
   auto* P = reinterpret_cast<double2*>(work);
-  switch (L) {
-    case 1: k_skinny<1><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
-    case 2: k_skinny<2><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
-    case 3: k_skinny<3><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
-    case 4: k_skinny<4><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
-    case 8: k_skinny<8><<<grid, SK_T, 0, st>>>(M, K, kchunk, Ad, lda, Bd, ldb, P); break;
-    default: throw CudaError("zgemm_skinny: L must be 1, 2, 3, 4 or 8");
-  }
+  if (a_c64)
+    skinny_launch(M, L, K, reinterpret_cast<const float2*>(A), lda, Bd, ldb, P, grid, kchunk, st);
+  else
+    skinny_launch(M, L, K, reinterpret_cast<const double2*>(A), lda, Bd, ldb, P, grid, kchunk, st);
   CHASE_CHECK_LAUNCH();
   const int64_t total = (int64_t)M * L;
   k_skinny_reduce<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, st>>>(

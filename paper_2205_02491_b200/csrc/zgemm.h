@@ -30,8 +30,9 @@ namespace chase {
 // Skinny product C[M x L] = alpha * A[M x K] * B[K x L] for L <= 8 (HBM-bound: streams A once;
 // used by the Lanczos step).  `work` must hold skinny_work_bytes(M, K, L).
 size_t skinny_work_bytes(int M, int K, int L);
+// a_c64: A is complex single (c64 shard), read and accumulated in FP64
 void zgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B,
-                  int64_t ldb, void* C, int64_t ldc, void* work, cudaStream_t st);
+                  int64_t ldb, void* C, int64_t ldc, void* work, cudaStream_t st, bool a_c64 = false);
 // real variant (f2); `work` as for the complex one (it needs half of it)
 void dgemm_skinny(int M, int L, int K, double alpha, const void* A, int64_t lda, const void* B,
                   int64_t ldb, void* C, int64_t ldc, void* work, cudaStream_t st);

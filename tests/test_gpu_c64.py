@@ -99,3 +99,47 @@ def test_c64_rejects_misaligned_shard(lib):
     Y = torch.zeros((8, 1001), dtype=torch.complex64, device="cuda").t()
     with pytest.raises(Exception):
         ch.hemm_step(0, H, X, Y, 8, 1.0, 0.0, 0.0)
+
+
+def test_c64_lanczos_vs_oracle(lib):
+    N, n_e = 700, 60
+    M = make_matrix("uniform", N, "g2", seed=4)
+    H = M.dense().astype(np.complex64)
+    ch = lib.Chase(N, 40, 20, dtype="c64")
+    b_sup, mu_1, mu_ne, nu = ch.lanczos(_dev(H), n_e)
+    lz = oracle.lanczos(H.astype(np.complex128), n_e)
+    # FP64-accumulated products on the fp32 shard: the bounds agree to the fp32 input rounding
+    for a, b in ((b_sup, lz.b_sup), (mu_1, lz.mu_1), (mu_ne, lz.mu_ne), (nu, lz.nu)):
+        assert abs(a - b) <= 1e-9 * max(1.0, abs(b)), (a, b)
+
+
+@pytest.mark.parametrize("fam,N", [("uniform", 600), ("wilkinson", 1000), ("121", 800)])
+def test_c64_solve_vs_exact(lib, fam, N):
+    """north_star: complex single eigenvalues to 1e-4 relative; here also 2e-5 ||H|| absolute and
+    the residuals of the returned complex64 vectors against the c64 shard in FP64."""
+    nev, nex = 40, 20
+    M = make_matrix(fam, N, "g2", seed=3)
+    H = M.dense().astype(np.complex64)
+    ch = lib.Chase(N, nev, nex, dtype="c64")
+    vals, dvecs, rep, st = ch.solve(_dev(H), nev, nex, deg=20, tol=1e-5)
+    assert st == 0, ch.last_error()
+    normH = np.max(np.abs(M.lam))
+    vecs = dvecs.cpu().numpy()[:, :nev].astype(np.complex128)
+    assert dvecs.dtype == torch.complex64
+    lam = M.lam[:nev]
+    assert np.max(np.abs(vals - lam) / np.maximum(np.abs(lam), 1e-300)) <= 1e-4 or \
+        np.max(np.abs(vals - lam)) <= 2e-5 * normH
+    assert np.max(np.abs(vals - lam)) <= 2e-5 * normH
+    Hd = H.astype(np.complex128)
+    res = np.linalg.norm(Hd @ vecs - vecs * vals[None, :], axis=0) / normH
+    assert np.max(res) <= 1e-4, np.max(res)
+    np.testing.assert_allclose(vecs.conj().T @ vecs, np.eye(nev), atol=1e-5)
+
+
+def test_c64_random_block_is_rounded_generator(lib):
+    from oracle.rng import random_block
+    N = 404
+    ch = lib.Chase(N, 10, 6, dtype="c64")
+    dV = torch.zeros((16, N), dtype=torch.complex64, device="cuda").t()
+    ch.random_block(dV, 3, 13, seed=99, stream=1)
+    assert np.array_equal(dV.cpu().numpy()[:, :13], random_block(99, 0, N, 3, 13, 1).astype(np.complex64))
