@@ -95,7 +95,12 @@ chase_status chase_init(chase_handle** out, const chase_init_args* args);
 /* Options (defaults): deg_max=36, max_iter=100, lanczos_steps=25, lanczos_runs=4, seed_v=2,
  * seed_lanczos=3, largest=0, approx=0 (1: ritz_vectors holds an initial V-hat on entry),
  * gemm3m=1 (filter and H*Q products use the 3M complex product -- 3 real DMMAs per complex
- * multiply-add instead of 4; normwise-stable; 0 selects the 4M kernel). */
+ * multiply-add instead of 4; normwise-stable; 0 selects the 4M kernel),
+ * mixed_filter=0 (CHASE_C128 only: a value r > 0 runs the filter of an iteration on a
+ * complex-single shadow of the shard -- the tcgen05 3xTF32 path, ~3.5x the FP64 filter rate --
+ * while every active column's residual is above r, with degrees aimed at max(tol, 1e-5); later
+ * iterations use the FP64 filter, so the returned pairs meet tol as usual.  Costs one extra
+ * shard-sized buffer (the complex64 shadow and its 3xTF32 low part)). */
 chase_status chase_set_option(chase_handle* h, const char* key, double value);
 
 /* This rank's shard: rows [row0, row0+p) and columns [col0, col0+q) of H. */

@@ -167,6 +167,22 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   }
   if (gamma == 0.0 || P.shift_lo >= P.shift_hi) P.shift_lo = P.shift_hi = 0;
   static bool attr[2] = {false, false};
+  static const bool pair = getenv("CHASE_C64_PAIR") && atoi(getenv("CHASE_C64_PAIR")) != 0;
+  if (pair) {
+    // CTA pairs: one cluster of 2 per 256-row x BN tile
+    constexpr size_t SMEM2 = Cfg2<BN>::SMEM;
+    static bool attr2[2] = {false, false};
+    const int grid2 = 2 * ceil_div(P.M, 2 * BMR) * ceil_div(P.N, BN);
+    if (dir == 0) {
+      if (!attr2[0]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel2<true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2)); attr2[0] = true; }
+      c64_step_kernel2<true, BN><<<grid2, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
+    } else {
+      if (!attr2[1]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel2<false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2)); attr2[1] = true; }
+      c64_step_kernel2<false, BN><<<grid2, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
+    }
+    CHASE_CHECK_LAUNCH();
+    return;
+  }
   const int grid = ceil_div(P.M, BMR) * ceil_div(P.N, BN);
   if (dir == 0) {
     if (!attr[0]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)); attr[0] = true; }
@@ -203,6 +219,21 @@ void allreduce_c64(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int
     CHASE_NCCL(ncclAllReduce(col, col, (size_t)(2 * rows), ncclFloat, ncclSum, comm, h->stream));
   }
   CHASE_NCCL(ncclGroupEnd());
+}
+
+// f4: complex64 shadow of a complex128 shard (rounded to nearest), ld p
+const void* c64_shadow(chase_handle* h, const void* H, int64_t ldh) {
+  const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
+  if (h->h32_src != H || h->h32_ld != ldh || !h->H32.p) {
+    h->H32.alloc(8 * (size_t)p * q);
+    k_convert<<<grid_for(p * q), 256, 0, h->stream>>>(h->H32.as<float2>(), p, reinterpret_cast<const double2*>(H), ldh,
+                                                      p, (int)q);
+    CHASE_CHECK_LAUNCH();
+    h->h32_src = H;
+    h->h32_ld = ldh;
+    h->hlo_src = nullptr;                   // the shadow's lo part must be rebuilt
+  }
+  return h->H32.p;
 }
 
 // H_lo for the shard (recomputed when the caller's H pointer or ld changes)

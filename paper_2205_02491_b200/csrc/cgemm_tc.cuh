@@ -101,6 +101,63 @@ __device__ __forceinline__ float tf32_lo(float x) {
 }
 }  // namespace tc
 
+// fused epilogue from the drained FP32 accumulators of one thread (one row, HN columns of each of
+// D1 / D2): shift on the intersection rows, scale, beta term, and the next step's operand formats
+template <bool FWD, int HN>
+__device__ __forceinline__ void c64_epilogue(const C64Params& p, int row, int nbase, const float (&a1)[HN],
+                                             const float (&a2)[HN]) {
+  const float ag = p.alpha * p.gamma;
+#pragma unroll
+  for (int j = 0; j < HN; ++j) {
+    const int n = nbase + j;
+    const float d1 = a1[j], d2 = a2[j];
+    if constexpr (FWD) {
+      // even lane (real row 2m): Re W = D1[2m] - D2[2m+1]; odd lane: Im W = D1[2m+1] + D2[2m]
+      const float d2p = __shfl_xor_sync(0xffffffffu, d2, 1);
+      const bool odd = (row & 1);
+      float v = odd ? (d1 + d2p) : (d1 - d2p);
+      v *= p.alpha;
+      const int mc = row >> 1;                         // complex row
+      if (n < p.N && row < p.M) {
+        if (mc >= p.shift_lo && mc < p.shift_hi) {
+          const float* src = odd ? p.S1 : p.S0;        // planar Re / Im of X
+          v -= ag * src[(int64_t)mc + p.shift_off + (int64_t)n * p.lds];
+        }
+        float* y = p.Y0 + (int64_t)row + (int64_t)n * p.ldy;
+        if (p.beta_on) v += p.beta * *y;
+      }
+      // rotated copy -i W: (Im, -Re) -> even lane takes Im from its partner, odd lane -Re
+      const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
+      if (n < p.N && row < p.M) {
+        const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
+        p.Y0[o] = v;
+        const float rot = odd ? -vp : vp;
+        if (p.Y1) p.Y1[o] = rot;
+        if (p.Y0lo) p.Y0lo[o] = tc::tf32_lo(v);
+        if (p.Y1lo) p.Y1lo[o] = tc::tf32_lo(rot);
+      }
+    } else {
+      if (n < p.N && row < p.M) {
+        float vr = p.alpha * d1, vi = p.alpha * d2;
+        if (row >= p.shift_lo && row < p.shift_hi) {
+          const float* src = p.S0 + 2 * ((int64_t)row + p.shift_off) + 2 * (int64_t)n * p.lds;   // interleaved X
+          vr -= ag * src[0];
+          vi -= ag * src[1];
+        }
+        const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
+        if (p.beta_on) {
+          vr += p.beta * p.Y0[o];
+          vi += p.beta * p.Y1[o];
+        }
+        p.Y0[o] = vr;
+        p.Y1[o] = vi;
+        if (p.Y0lo) p.Y0lo[o] = tc::tf32_lo(vr);
+        if (p.Y1lo) p.Y1lo[o] = tc::tf32_lo(vi);
+      }
+    }
+  }
+}
+
 // FWD = true: forward step (A MN-major from H, output W interleaved + rotated + lo copies)
 // FWD = false: backward step (A K-major from H's columns, output V planar + lo planes)
 //
@@ -262,60 +319,228 @@ __global__ void __launch_bounds__(C64_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + b);
     }
-    const float ag = p.alpha * p.gamma;
-#pragma unroll
-    for (int j = 0; j < HN; ++j) {
-      const int n = n0 + half * HN + j;
-      const float d1 = a1[j], d2 = a2[j];
-      if constexpr (FWD) {
-        // even lane (real row 2m): Re W = D1[2m] - D2[2m+1]; odd lane: Im W = D1[2m+1] + D2[2m]
-        const float d2p = __shfl_xor_sync(0xffffffffu, d2, 1);
-        const bool odd = (row & 1);
-        float v = odd ? (d1 + d2p) : (d1 - d2p);
-        v *= p.alpha;
-        const int mc = row >> 1;                         // complex row
-        if (n < p.N && row < p.M) {
-          if (mc >= p.shift_lo && mc < p.shift_hi) {
-            const float* src = odd ? p.S1 : p.S0;        // planar Re / Im of X
-            v -= ag * src[(int64_t)mc + p.shift_off + (int64_t)n * p.lds];
-          }
-          float* y = p.Y0 + (int64_t)row + (int64_t)n * p.ldy;
-          if (p.beta_on) v += p.beta * *y;
-        }
-        // rotated copy -i W: (Im, -Re) -> even lane takes Im from its partner, odd lane -Re
-        const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
-        if (n < p.N && row < p.M) {
-          const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
-          p.Y0[o] = v;
-          const float rot = odd ? -vp : vp;
-          if (p.Y1) p.Y1[o] = rot;
-          if (p.Y0lo) p.Y0lo[o] = tc::tf32_lo(v);
-          if (p.Y1lo) p.Y1lo[o] = tc::tf32_lo(rot);
-        }
-      } else {
-        if (n < p.N && row < p.M) {
-          float vr = p.alpha * d1, vi = p.alpha * d2;
-          if (row >= p.shift_lo && row < p.shift_hi) {
-            const float* src = p.S0 + 2 * ((int64_t)row + p.shift_off) + 2 * (int64_t)n * p.lds;   // interleaved X
-            vr -= ag * src[0];
-            vi -= ag * src[1];
-          }
-          const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
-          if (p.beta_on) {
-            vr += p.beta * p.Y0[o];
-            vi += p.beta * p.Y1[o];
-          }
-          p.Y0[o] = vr;
-          p.Y1[o] = vi;
-          if (p.Y0lo) p.Y0lo[o] = tc::tf32_lo(vr);
-          if (p.Y1lo) p.Y1lo[o] = tc::tf32_lo(vi);
-        }
-      }
-    }
+    c64_epilogue<FWD, HN>(p, row, n0 + half * HN, a1, a2);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(TCOLS));
+}
+
+// ============================================================================================
+// CTA-pair variant (tcgen05 cta_group::2): the two CTAs of a cluster share one M = 256 x N = 2BN
+// MMA.  Each CTA stages its own 128 A rows and HALF of [B1 | B2] (rank 0: B1, rank 1: B2), so per
+// CTA a stage is 64 KB instead of 96 KB (3 stages fit) and the L2 -> SM tile traffic drops by 1/3.
+// The leader (rank 0) issues the MMAs; both CTAs' TMA loads complete on the leader's `full`
+// barrier; MMA commits are multicast to both CTAs' `empty` / `acc_full` barriers; the 16 drain
+// warps of the pair arrive on the leader's `acc_empty`.  Each CTA's TMEM holds its 128 rows of
+// D = [A B1 | A B2], so the drain / epilogue code is the single-CTA one.
+namespace tc2 {
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAITC:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONEC;\n"
+      "bra LAB_WAITC;\n"
+      "DONEC:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p; }"
+               ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit_both(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+}  // namespace tc2
+
+template <int BN>
+struct Cfg2 {
+  static constexpr uint32_t B_BYTES = tc::BK * BN * 4;                       // one CTA's B half
+  static constexpr uint32_t STAGE_BYTES = 2 * tc::A_BYTES + 2 * B_BYTES;   // A hi/lo + B half hi/lo
+  static constexpr int STAGES = (220 * 1024) / STAGE_BYTES > 4 ? 4 : (220 * 1024) / STAGE_BYTES;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+};
+
+template <bool FWD, int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
+    c64_step_kernel2(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tAlo,
+                     const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB1lo,
+                     const __grid_constant__ CUtensorMap tB2, const __grid_constant__ CUtensorMap tB2lo,
+                     C64Params p) {
+  using namespace tc;
+  constexpr uint32_t B_BYTES = Cfg2<BN>::B_BYTES, STAGE_BYTES = Cfg2<BN>::STAGE_BYTES;
+  constexpr int STAGES = Cfg2<BN>::STAGES;
+  const int CH = p.kc_stages > 0 ? p.kc_stages : C64_KC_STAGES;
+  constexpr uint32_t TCOLS = 4 * BN;
+  constexpr int HN = BN / 2;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc2::cluster_rank();
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int pair = blockIdx.x >> 1;
+  const int m0 = (pair / tiles_n) * (2 * BMR) + (int)rank * BMR;
+  const int n0 = (pair % tiles_n) * BN;
+  const int KT = (p.K + BK - 1) / BK;
+  const int NCH = (KT + CH - 1) / CH;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 16);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  tc2::cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer (both CTAs)
+      tma_prefetch_desc(&tA);
+      tma_prefetch_desc(rank == 0 ? &tB1 : &tB2);
+      const CUtensorMap* tb = rank == 0 ? &tB1 : &tB2;
+      const CUtensorMap* tbl = rank == 0 ? &tB1lo : &tB2lo;
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(empty + s, ((kt / STAGES) - 1) & 1);
+        const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+        const uint32_t fb = tc2::mapa(smem_u32(full + s), 0);
+        if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * STAGE_BYTES);
+        const int k0 = kt * BK;
+        if constexpr (FWD) {
+#pragma unroll
+          for (int c = 0; c < BMR / 32; ++c) {
+            tc2::tma_load_2d_pair(st + c * (BK * 128), &tA, m0 + 32 * c, k0, fb);
+            tc2::tma_load_2d_pair(st + A_BYTES + c * (BK * 128), &tAlo, m0 + 32 * c, k0, fb);
+          }
+        } else {
+          tc2::tma_load_2d_pair(st, &tA, k0, m0, fb);
+          tc2::tma_load_2d_pair(st + A_BYTES, &tAlo, k0, m0, fb);
+        }
+        tc2::tma_load_2d_pair(st + 2 * A_BYTES, tb, k0, n0, fb);
+        tc2::tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, tbl, k0, n0, fb);
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // -------------------------------------------------------------- MMA issuer (leader CTA)
+      uint32_t leader;
+      asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((FWD ? 1u : 0u) << 15) |
+                             ((uint32_t)((2 * BN) >> 3) << 17) | ((uint32_t)((2 * BMR) >> 4) << 24);
+      for (int kt = 0; kt < KT; ++kt) {
+        const int s = kt % STAGES;
+        const int chunk = kt / CH, b = chunk & 1;
+        const bool chunk_start = (kt % CH) == 0;
+        if (chunk_start && chunk >= 2) {
+          tc2::wait_cluster(acc_empty + b, ((chunk >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        mbar_wait(full + s, (kt / STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (leader) {
+          const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+          const uint32_t sa = st, salo = st + A_BYTES, sb = st + 2 * A_BYTES;
+          const uint32_t td = tm + (uint32_t)b * 2 * BN;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            uint64_t da, dal;
+            if constexpr (FWD) {
+              da = sdesc(sa + kk * 1024, BK * 128, 512, 1);
+              dal = sdesc(salo + kk * 1024, BK * 128, 512, 1);
+            } else {
+              da = sdesc(sa + kk * 32, 16, 1024, 2);
+              dal = sdesc(salo + kk * 32, 16, 1024, 2);
+            }
+            const uint64_t db = sdesc(sb + kk * 32, 16, 1024, 2);
+            const uint64_t dbl = sdesc(sb + B_BYTES + kk * 32, 16, 1024, 2);
+            const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
+            tc2::mma_tf32(td, da, db, idesc, acc);
+            tc2::mma_tf32(td, da, dbl, idesc, 1u);
+            tc2::mma_tf32(td, dal, db, idesc, 1u);
+          }
+          tc2::commit_both(empty + s);
+          if ((kt % CH) == CH - 1 || kt == KT - 1) tc2::commit_both(acc_full + b);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ drain + epilogue (8 warps)
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row = m0 + 32 * quad + lane;
+    const uint32_t lane_base = tm + ((uint32_t)(32 * quad) << 16) + (uint32_t)(half * HN);
+    float a1[HN], a2[HN];
+#pragma unroll
+    for (int j = 0; j < HN; ++j) a1[j] = a2[j] = 0.f;
+    for (int chunk = 0; chunk < NCH; ++chunk) {
+      const int b = chunk & 1;
+      mbar_wait(acc_full + b, (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t base = lane_base + (uint32_t)b * 2 * BN;
+#pragma unroll
+      for (int c0 = 0; c0 < HN; c0 += 16) {
+        uint32_t r1[16], r2[16];
+        tc::ld16(base + c0, r1);
+        tc::ld16(base + BN + c0, r2);
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          a1[c0 + j] += __uint_as_float(r1[j]);
+          a2[c0 + j] += __uint_as_float(r2[j]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) tc2::arrive_cluster(tc2::mapa(smem_u32(acc_empty + b), 0));
+    }
+    c64_epilogue<FWD, HN>(p, row, n0 + half * HN, a1, a2);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  tc2::cluster_sync();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(TCOLS));
 }
 
 }  // namespace chase

@@ -400,6 +400,7 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     else if (k == "largest") h->opt.largest = v != 0.0;
     else if (k == "approx") h->opt.approx = v != 0.0;
     else if (k == "gemm3m") h->opt.gemm3m = v != 0.0;
+    else if (k == "mixed_filter") h->opt.mixed_filter = v;
     else throw UsageError("unknown option " + k);
     return CHASE_OK;
   }, false);
@@ -507,7 +508,7 @@ chase_status chase_finalize(chase_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo,
-                         &h->c64v, &h->c64w})
+                         &h->c64v, &h->c64w, &h->H32})
     b->release();
   if (h->rowc) ncclCommDestroy(h->rowc);
   if (h->colc) ncclCommDestroy(h->colc);

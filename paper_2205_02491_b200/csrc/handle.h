@@ -59,6 +59,7 @@ struct Options {
   bool largest = false;
   bool approx = false;
   bool gemm3m = true;         // 3M complex products in the filter / HQ GEMMs
+  double mixed_filter = 0.0;  // f4: complex-single filter while all active residuals exceed this
 };
 
 }  // namespace chase
@@ -81,6 +82,9 @@ struct chase_handle {
   chase::DBuf V, W, HV, V2, G, G2, Z, scratch, red, lz;
   chase::DBuf Hlo;                     // c64: 3xTF32 lo part of the caller's H shard
   chase::DBuf c64v, c64w;              // c64: planar V-layout / W-layout operand formats (c64.cu)
+  chase::DBuf H32;                     // f4: complex-single shadow of a complex-double shard
+  const void* h32_src = nullptr;
+  int64_t h32_ld = 0;
   const void* hlo_src = nullptr;
   int64_t hlo_ld = 0;
   std::vector<double> host_scratch;
@@ -122,6 +126,8 @@ void c64_hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const v
                    int64_t ldy, int ncols, double alpha, double beta, double gamma);
 int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, int ncols, const int* degrees,
                    double b_sup, double mu_1, double mu_ne);
+// f4: complex64 shadow (ld p) of a complex128 shard, rebuilt when H / ldh change
+const void* c64_shadow(chase_handle* h, const void* H, int64_t ldh);
 // H_lo of the shard (validates the c64 layout; recomputed when H / ldh change)
 const void* c64_hlo(chase_handle* h, const void* H, int64_t ldh);
 // mixed solve (c64 shard, complex128 iteration): filter / HX on complex128 blocks, and conversions

@@ -151,6 +151,18 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
   // kernels (tcgen05 3xTF32 filter / HQ, FP64-accumulated skinny Lanczos product), the iteration
   // around it (QR, RR, residuals) in complex double on the handle's workspace.
   const bool mixed = h->c64();
+  // f4: complex-double solve whose early filters run on a complex-single shadow
+  bool f4 = false;
+  const void* H32 = nullptr;
+  if constexpr (SC<T>::is_complex) {
+    if (!mixed && h->opt.mixed_filter > 0.0) {
+      H32 = c64_shadow(h, Hv, ldh);
+      c64_hlo(h, H32, p);                       // validates the layout up front
+      f4 = true;
+    }
+  }
+  constexpr double kC64Floor = 1e-5;            // residual level the c64 filter can reach
+  bool f4_next = f4;                             // iteration 1 starts from random vectors
   // ---- initial V-hat (Require of Alg. 1)
   if (h->opt.approx && mixed)
     c64_convert(V, q, true, ritz_vectors, ldv_out, q, n_e, st);
@@ -174,9 +186,12 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
 
     // ---- line 4: Filter
     t_f.start(st);
+    const bool f4_now = f4 && f4_next;
     if constexpr (SC<T>::is_complex) {
       if (mixed)
         matvecs += c64_filter_mixed(h, Hv, ldh, Va, q, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
+      else if (f4_now)
+        matvecs += c64_filter_mixed(h, H32, p, Va, q, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
       else
         matvecs += filter(h, Hv, ldh, Va, q, Wa, p, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
     } else {
@@ -296,6 +311,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
       ritz[locked + a] = th_h[a];
       res[locked + a] = std::sqrt(std::max(0.0, r2_h[a])) / nu;
     }
+    if (trace && g.rank == 0 && f4) std::fprintf(stderr, "[chase] it=%d filter=%s\n", it, f4_now ? "c64" : "c128");
     if (trace && g.rank == 0) {
       double rmin = 1e300, rmax = 0.0;
       for (int a = 0; a < n_act; ++a) { rmin = std::min(rmin, res[locked + a]); rmax = std::max(rmax, res[locked + a]); }
@@ -313,10 +329,19 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     mu_ne = *std::max_element(ritz.begin(), ritz.end());
     const double c = 0.5 * (b_sup + mu_ne), e = 0.5 * (b_sup - mu_ne);
     if (locked >= nev) break;
+    // f4: next filter in complex single while every active residual is above the threshold;
+    // its degrees then aim at what complex single can reach
+    double tol_deg = tol;
+    if (f4) {
+      double rmin = 1e300;
+      for (int a = locked; a < n_e; ++a) rmin = std::min(rmin, res[a]);
+      f4_next = rmin > h->opt.mixed_filter;
+      if (f4_next) tol_deg = std::max(tol, kC64Floor);
+    }
     // ---- lines 11-14: degrees, stable sort by degree
     const int na = n_e - locked;
     std::vector<int> mm(na), perm(na);
-    for (int a = 0; a < na; ++a) mm[a] = optimal_degree(tol, res[locked + a], ritz[locked + a], c, e, deg_max);
+    for (int a = 0; a < na; ++a) mm[a] = optimal_degree(tol_deg, res[locked + a], ritz[locked + a], c, e, deg_max);
     std::iota(perm.begin(), perm.end(), 0);
     std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return mm[x] < mm[y]; });
     std::vector<double> rz(na), rs(na);

@@ -143,3 +143,22 @@ def test_c64_random_block_is_rounded_generator(lib):
     dV = torch.zeros((16, N), dtype=torch.complex64, device="cuda").t()
     ch.random_block(dV, 3, 13, seed=99, stream=1)
     assert np.array_equal(dV.cpu().numpy()[:, :13], random_block(99, 0, N, 3, 13, 1).astype(np.complex64))
+
+
+@pytest.mark.parametrize("fam,N", [("uniform", 1200), ("wilkinson", 1000)])
+def test_f4_mixed_filter_c128_solve(lib, fam, N):
+    """complex-double solve whose early filters run on the complex-single shadow; the
+    returned pairs must meet the complex-double bars exactly as without it."""
+    nev, nex = 40, 20
+    M = make_matrix(fam, N, "g2", seed=3)
+    H = M.dense()
+    dH = torch.from_numpy(np.asfortranarray(H)).t().contiguous().t().cuda()
+    ch = lib.Chase(N, nev, nex)
+    ch.set_option("mixed_filter", 1e-3)
+    vals, dvecs, rep, st = ch.solve(dH, nev, nex, deg=20, tol=1e-10)
+    assert st == 0, ch.last_error()
+    normH = np.max(np.abs(M.lam))
+    vecs = dvecs.cpu().numpy()[:, :nev]
+    assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
+    assert np.max(np.linalg.norm(H @ vecs - vecs * vals[None, :], axis=0)) <= 1e-10 * normH
+    np.testing.assert_allclose(vecs.conj().T @ vecs, np.eye(nev), atol=1e-12)

@@ -23,12 +23,15 @@ if single:
 dtype = "r64" if real else ("c64" if single else "c128")
 ch = pkg.Chase(N, nev, nex, dtype=dtype)
 ch.set_option("max_iter", int(sys.argv[5]) if len(sys.argv) > 5 else 100)
+import os
+if os.environ.get("CHASE_MIXED"):
+    ch.set_option("mixed_filter", float(os.environ["CHASE_MIXED"]))
 vals, vecs, rep, st = ch.solve(H, nev, nex, deg=20, tol=tol)
 normH = np.max(np.abs(M.lam))
 print(json.dumps({"N": N, "nev": nev, "nex": nex, "family": fam, "status": st, "t_all": rep["t_all"],
                   "iterations": rep["iterations"], "matvecs": rep["matvecs"],
                   "phases": {k: rep[k] for k in ("t_lanczos", "t_filter", "t_qr", "t_rr", "t_resid")},
-                  "dtype": dtype, "tol": tol,
+                  "dtype": dtype, "tol": tol, "mixed_filter": float(os.environ.get("CHASE_MIXED", "0")),
                   "filter_tflops": rep["filter_flops"] / max(rep["t_filter"], 1e-12) / 1e12,
                   "eig_err_rel": float(np.max(np.abs(vals - M.lam[:nev])) / normH),
                   "eig_err_relmax": float(np.max(np.abs(vals - M.lam[:nev]) / np.abs(M.lam[:nev])))}))
