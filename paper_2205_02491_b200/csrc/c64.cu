@@ -167,7 +167,8 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   }
   if (gamma == 0.0 || P.shift_lo >= P.shift_hi) P.shift_lo = P.shift_hi = 0;
   static bool attr[2] = {false, false};
-  static const bool pair = getenv("CHASE_C64_PAIR") && atoi(getenv("CHASE_C64_PAIR")) != 0;
+  // CTA pairs (default; CHASE_C64_PAIR=0 selects the single-CTA kernel)
+  static const bool pair = !getenv("CHASE_C64_PAIR") || atoi(getenv("CHASE_C64_PAIR")) != 0;
   if (pair) {
     // CTA pairs: one cluster of 2 per 256-row x BN tile
     constexpr size_t SMEM2 = Cfg2<BN>::SMEM;
