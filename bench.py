@@ -36,6 +36,9 @@ FP64_DMMA_PEAK_TFLOPS = 37.12     # measured (profiles/r01_fp64_peak.jsonl), see
 # The filter GEMM uses the 3M complex product (3 real DMMA per complex multiply-add), so its
 # ceiling in algorithmic complex flops (8 per complex MAC) is 4/3 of the DMMA peak.
 FILTER_PEAK_3M_TFLOPS = FP64_DMMA_PEAK_TFLOPS * 4.0 / 3.0
+# Complex single (tcgen05 kind::tf32, 3xTF32): TF32 dense peak = 1/2 x the measured BF16 peak
+# (MEASURED_PEAKS.json, nominal ratio of the profiling guide); 3 MMAs per real product -> /3.
+BF16_MEASURED_TFLOPS = 1644.0
 METRIC = "filter TFLOP/s, one ChASE subspace iteration (P:727-731), complex double"
 
 
@@ -52,6 +55,7 @@ def parse():
     ap.add_argument("--tts", action="store_true", help="also run a full solve to convergence (time-to-solution)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c64", action="store_true", help="skip the complex-single filter sub-measurement")
     return ap.parse_args()
 
 
@@ -290,6 +294,41 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # ---- complex-single filter on the same workload shape: H rounded to
+    #      complex64 once (untimed), chase_filter with every column at degree 20 (20 fused steps)
+    c64 = None
+    if world == 1 and not args.no_c64:
+        try:
+            bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", BF16_MEASURED_TFLOPS)
+        except Exception:
+            bf16 = BF16_MEASURED_TFLOPS
+        peak64 = bf16 * 0.5 / 3.0
+        H32 = H.to(torch.complex64)
+        ch32 = pkg.Chase(N, nev, nex, dtype="c64", device=local, stream=stream)
+        V32 = (vecs[:, :nev + nex]).to(torch.complex64)
+        W32 = torch.empty((nev + nex, p), dtype=torch.complex64, device="cuda").t()
+        degs = [DEG] * (nev + nex)
+        lam = M.lam
+        b_sup, mu_1, mu_ne = float(lam[-1]) * 1.05, float(lam[0]), float(lam[nev + nex])
+        ch32.filter(H32, V32, W32, degs, b_sup, mu_1, mu_ne)          # warm-up (+ H_lo, formats)
+        reps64 = 3
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        mv64 = 0
+        for _ in range(reps64):
+            mv64 += ch32.filter(H32, V32, W32, degs, b_sup, mu_1, mu_ne)
+        e1.record()
+        torch.cuda.synchronize()
+        t64 = e0.elapsed_time(e1) * 1e-3
+        a64 = 8.0 * N * N * mv64 / t64 / 1e12
+        c64 = {"what": "chase_filter in complex single (CHASE_C64: tcgen05 kind::tf32 3xTF32 on CTA pairs), "
+                       f"N={N}, {nev + nex} columns at degree {DEG}, same Uniform H rounded to complex64",
+               "tflops": a64, "peak": peak64, "frac": a64 / peak64, "unit": "TFLOP/s", "s_per_filter": t64 / reps64,
+               "peak_source": f"1/2 x measured BF16 {bf16} TFLOP/s (TF32 nominal ratio) / 3 MMAs per real product"}
+        ch32.close()
+        del H32, V32, W32
+        torch.cuda.empty_cache()
     tts = None
     if args.tts:
         ch.set_option("max_iter", 100)
@@ -321,6 +360,8 @@ def main():
                 "clocks": clocks, "gpu_launches": launches, "e2e": e2e}
         if tts:
             line["time_to_solution"] = tts
+        if c64:
+            line["c64_filter"] = c64
         if world == 1 and not args.no_cpu:
             v, cores, sample = oracle_sample(N, seconds=12.0, family=args.family)
             line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
