@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include "dense.h"
 #include "handle.h"
 #include "linalg.h"
 #include "rng.cuh"
@@ -128,6 +129,16 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
     if (const char* env = std::getenv("CHASE_FILTER_CHUNKS"))      // testing / tuning override
       nchunks = std::max(1, std::min({chase_handle::MAX_CHUNKS, ncols, std::atoi(env)}));
   }
+  // f1: all-reduce inside the GEMM over peer memory (internal V / W buffers only: the peers'
+  // replicas are the handles' workspace at the same offsets)
+  auto inside = [](const DBuf& b, const void* ptr) {
+    const char* c = reinterpret_cast<const char*>(ptr);
+    const char* s = reinterpret_cast<const char*>(b.p);
+    return b.p && c >= s && c < s + b.bytes;
+  };
+  const bool fused = comm && ldv == g.cols.len && ldw == g.rows.len && inside(h->V, V) && inside(h->W, W) &&
+                     peer_reduce_ready(h);
+  if (fused) nchunks = 1;
   std::vector<int> bnd(nchunks + 1);
   for (int c = 0; c <= nchunks; ++c) bnd[c] = (int)((int64_t)ncols * c / nchunks);
   bool rec[2][chase_handle::MAX_CHUNKS] = {};
@@ -153,6 +164,19 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
                 ncols - first, alpha, beta, c);
       continue;
     }
+    if (fused) {
+      char* Yk = Y + (int64_t)first * ldy * es;
+      ZgemmDesc d = step_desc(h, dir, H, ldh, X + (int64_t)first * ldx * es, ldx, Yk, ldy, ncols - first, alpha,
+                              beta, c);
+      d.red = peer_red_for(h, dir, Yk);
+      if (d.red) {
+        gemm(h, d);
+        peer_wait(h, zgemm3m_tiles(d.M, d.N));
+      } else {                                   // this direction's communicator has one rank
+        gemm(h, d);
+      }
+      continue;
+    }
     const int64_t rows = dir == 0 ? g.rows.len : g.cols.len;
     for (int ch = 0; ch < nchunks; ++ch) {
       const int lo = std::max(first, bnd[ch]), hi = bnd[ch + 1];
@@ -174,7 +198,9 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       rec[(k - 1) & 1][ch] = false;
     }
   }
-  if (comm) {
+  if (fused) {
+    peer_check(h);
+  } else if (comm) {
     CHASE_CUDA(cudaEventRecord(h->ev_join, h->comm_stream));
     CHASE_CUDA(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   }
@@ -401,6 +427,7 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     else if (k == "approx") h->opt.approx = v != 0.0;
     else if (k == "gemm3m") h->opt.gemm3m = v != 0.0;
     else if (k == "mixed_filter") h->opt.mixed_filter = v;
+    else if (k == "fused_reduce") h->opt.fused_reduce = v != 0.0;
     else throw UsageError("unknown option " + k);
     return CHASE_OK;
   }, false);
@@ -442,8 +469,20 @@ chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, 
     if (!H || !V || !W || ncols < 0 || (ncols > 0 && !degrees)) throw UsageError("bad pointers");
     if (ldh < p || ldv < q || ldw < p) throw UsageError("bad leading dimension");
     order_after_user(h);
-    const int64_t mv = h->c64() ? c64_filter(h, H, ldh, V, ldv, ncols, degrees, b_sup, mu_1, mu_ne)
-                                : filter(h, H, ldh, V, ldv, W, ldw, ncols, degrees, b_sup, mu_1, mu_ne);
+    const Grid& g = h->grid;
+    // f1 runs on the library's V / W workspace (the peers' replicas): stage the caller's block
+    const bool staged = h->dtype == CHASE_C128 && h->opt.fused_reduce && h->opt.gemm3m && h->world_size > 1 &&
+                        (g.r > 1 || g.c > 1) && ncols > 0 && ncols <= h->n_e_max;
+    int64_t mv;
+    if (h->c64()) {
+      mv = c64_filter(h, H, ldh, V, ldv, ncols, degrees, b_sup, mu_1, mu_ne);
+    } else if (staged) {
+      copy2d<double2>(h->V.p, q, V, ldv, q, ncols, h->stream);
+      mv = filter(h, H, ldh, h->V.p, q, h->W.p, p, ncols, degrees, b_sup, mu_1, mu_ne);
+      copy2d<double2>(V, ldv, h->V.p, q, q, ncols, h->stream);
+    } else {
+      mv = filter(h, H, ldh, V, ldv, W, ldw, ncols, degrees, b_sup, mu_1, mu_ne);
+    }
     CHASE_CUDA(cudaStreamSynchronize(h->stream));
     if (matvecs) *matvecs = mv;
     return CHASE_OK;
@@ -507,6 +546,7 @@ chase_status chase_finalize(chase_handle* h) {
   if (!h) return CHASE_E_USAGE;
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  chase::peer_release(h);
   for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo,
                          &h->c64v, &h->c64w, &h->H32})
     b->release();

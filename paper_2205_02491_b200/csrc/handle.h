@@ -60,6 +60,7 @@ struct Options {
   bool approx = false;
   bool gemm3m = true;         // 3M complex products in the filter / HQ GEMMs
   double mixed_filter = 0.0;  // f4: complex-single filter while all active residuals exceed this
+  bool fused_reduce = true;   // f1: filter steps all-reduce inside the GEMM over peer memory
 };
 
 }  // namespace chase
@@ -95,6 +96,16 @@ struct chase_handle {
   static constexpr int MAX_CHUNKS = 8;
   cudaEvent_t ev_gemm[MAX_CHUNKS] = {}, ev_comm[2][MAX_CHUNKS] = {}, ev_join = nullptr;
   bool broken = false;
+  // f1: fused all-reduce over peer memory (peer.cu)
+  struct Peer {
+    bool ready = false, failed = false;
+    chase::DBuf stage, ctr;
+    unsigned* done_local = nullptr;
+    unsigned* err = nullptr;
+    unsigned expected = 0;
+    chase::PeerRed row, col;
+    std::vector<void*> opened;
+  } peer;
 };
 
 namespace chase {
@@ -137,6 +148,13 @@ void c64_forward_mixed(chase_handle* h, const void* H, int64_t ldh, const double
                        int64_t ldy, int ncols);
 void c64_convert(void* dst, int64_t ldd, bool dst_c128, const void* src, int64_t lds, int64_t rows, int cols,
                  cudaStream_t st);
+
+// f1 (peer.cu): set up / use the fused peer all-reduce of the filter steps
+bool peer_reduce_ready(chase_handle* h);
+const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y);
+void peer_wait(chase_handle* h, int tiles);
+void peer_check(chase_handle* h);
+void peer_release(chase_handle* h);
 
 chase_status solve(chase_handle* h, const void* H, int64_t ldh, int nev, int nex, int deg,
                    double tol, double* ritz_values, void* ritz_vectors, int64_t ldv,

@@ -1,0 +1,156 @@
+// f1: the fused steps' all-reduce over peer memory instead of NCCL.
+//
+// Setup (once per handle, collective over the row and column communicators): a staging buffer
+// (16 B x max(p, q) x n_e), tile-arrival counters and a completion counter are allocated; their
+// CUDA IPC handles, and those of the V / W workspace replicas, are all-gathered over each
+// communicator (ncclAllGather of the 64-byte handles) and opened, so every rank holds device
+// pointers to its row peers' W and staging buffers and its column peers' V and staging buffers.
+// NVLink5 / NVSwitch carries the peer loads and stores issued by the GEMM epilogue
+// (zgemm3m.cuh).  After each fused step a one-thread kernel waits on the local completion
+// counter, which the reducers bump once per tile, so the next step reads a complete replica.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include "handle.h"
+
+namespace chase {
+
+namespace {
+constexpr int kCtrPerComm = 1 << 17;          // tile counters per communicator (> max tiles per step)
+
+__global__ void k_wait_done(const unsigned* done, unsigned target, unsigned* err, unsigned long long timeout_ns) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if ((int)(v - target) >= 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      atomicExch(err, 1u);
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
+struct Handles {
+  cudaIpcMemHandle_t stage, vec, ctr;
+};
+
+// all-gather `mine` over `comm` (size n) -> out[n]
+void gather_handles(chase_handle* h, ncclComm_t comm, int n, const Handles& mine, std::vector<Handles>& out) {
+  out.assign(n, Handles{});
+  void* d = nullptr;
+  CHASE_CUDA(cudaMalloc(&d, sizeof(Handles) * (n + 1)));
+  CHASE_CUDA(cudaMemcpyAsync(d, &mine, sizeof(Handles), cudaMemcpyHostToDevice, h->stream));
+  CHASE_NCCL(ncclAllGather(d, reinterpret_cast<char*>(d) + sizeof(Handles), sizeof(Handles), ncclUint8, comm,
+                           h->stream));
+  CHASE_CUDA(cudaMemcpyAsync(out.data(), reinterpret_cast<char*>(d) + sizeof(Handles), sizeof(Handles) * n,
+                             cudaMemcpyDeviceToHost, h->stream));
+  CHASE_CUDA(cudaStreamSynchronize(h->stream));
+  cudaFree(d);
+}
+
+void* open_peer(chase_handle* h, const cudaIpcMemHandle_t& hd) {
+  void* p = nullptr;
+  CHASE_CUDA(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+  h->peer.opened.push_back(p);
+  return p;
+}
+}  // namespace
+
+bool peer_reduce_ready(chase_handle* h) {
+  const Grid& g = h->grid;
+  if (h->peer.failed || !h->opt.fused_reduce || h->dtype != CHASE_C128 || !h->opt.gemm3m) return false;
+  if (h->world_size <= 1 || !h->world || (g.r <= 1 && g.c <= 1)) return false;
+  if (g.r > kMaxPeers || g.c > kMaxPeers) return false;
+  if (h->peer.ready) return true;
+  // ---- collective setup (every rank of the grid reaches this point with the same options)
+  const int64_t p = g.rows.len, q = g.cols.len, ne = h->n_e_max;
+  h->peer.stage.alloc(16 * (size_t)std::max(p, q) * ne);
+  h->peer.ctr.alloc(sizeof(unsigned) * (2 * (size_t)kCtrPerComm + 64));
+  CHASE_CUDA(cudaMemsetAsync(h->peer.ctr.p, 0, h->peer.ctr.bytes, h->stream));
+  unsigned* base = h->peer.ctr.as<unsigned>();
+  h->peer.done_local = base + 2 * kCtrPerComm;
+  h->peer.err = base + 2 * kCtrPerComm + 32;
+  Handles row_mine{}, col_mine{};
+  CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.stage, h->peer.stage.p));
+  CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.ctr, h->peer.ctr.p));
+  col_mine = row_mine;
+  CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.vec, h->W.p));      // row comm sums W-layout blocks
+  CHASE_CUDA(cudaIpcGetMemHandle(&col_mine.vec, h->V.p));      // column comm sums V-layout blocks
+  std::vector<Handles> rows_h, cols_h;
+  if (g.c > 1) gather_handles(h, h->rowc, g.c, row_mine, rows_h);
+  if (g.r > 1) gather_handles(h, h->colc, g.r, col_mine, cols_h);
+  auto fill = [&](PeerRed& pr, int n, int me, const std::vector<Handles>& hs, void* own_vec, int ctr_slot) {
+    pr.n = n;
+    pr.me = me;
+    std::vector<unsigned*> ctrs(n);
+    for (int r = 0; r < n; ++r) {
+      if (r == me) {
+        pr.stage[r] = h->peer.stage.as<double2>();
+        pr.out[r] = reinterpret_cast<double2*>(own_vec);
+        ctrs[r] = base;
+      } else {
+        pr.stage[r] = reinterpret_cast<double2*>(open_peer(h, hs[r].stage));
+        pr.out[r] = reinterpret_cast<double2*>(open_peer(h, hs[r].vec));
+        ctrs[r] = reinterpret_cast<unsigned*>(open_peer(h, hs[r].ctr));
+      }
+      pr.done[r] = ctrs[r] + 2 * kCtrPerComm;
+    }
+    pr.ctr = ctrs[0] + (size_t)ctr_slot * kCtrPerComm;        // owned by comm rank 0
+  };
+  // rank within the row comm = j (split key j), within the column comm = i (key i)
+  if (g.c > 1) fill(h->peer.row, g.c, g.j, rows_h, h->W.p, 0);
+  if (g.r > 1) fill(h->peer.col, g.r, g.i, cols_h, h->V.p, 1);
+  CHASE_CUDA(cudaStreamSynchronize(h->stream));
+  // barrier over the world (sum of the zeroed error words): every rank's counters are zeroed before
+  // anyone may arrive on them
+  CHASE_NCCL(ncclAllReduce(h->peer.err, h->peer.err, 1, ncclUint32, ncclSum, h->world, h->stream));
+  CHASE_CUDA(cudaStreamSynchronize(h->stream));
+  h->peer.expected = 0;
+  h->peer.ready = true;
+  if (std::getenv("CHASE_DEBUG_PEER"))
+    std::fprintf(stderr, "[chase] rank %d: fused peer all-reduce ready (row comm %d, column comm %d)\n", g.rank,
+                 h->peer.row.n, h->peer.col.n);
+  return true;
+}
+
+// launch-side helpers for one fused step on the internal buffers: `Y` lies in h->W (dir 0) or h->V
+const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y) {
+  PeerRed& pr = dir == 0 ? h->peer.row : h->peer.col;
+  if (pr.n <= 1) return nullptr;
+  const char* base = reinterpret_cast<const char*>(dir == 0 ? h->W.p : h->V.p);
+  pr.off = (reinterpret_cast<const char*>(Y) - base) / 16;
+  return &pr;
+}
+
+void peer_wait(chase_handle* h, int tiles) {
+  h->peer.expected += (unsigned)tiles;
+  k_wait_done<<<1, 1, 0, h->stream>>>(h->peer.done_local, h->peer.expected, h->peer.err, 20ull * 1000000000ull);
+  CHASE_CHECK_LAUNCH();
+}
+
+void peer_check(chase_handle* h) {
+  if (!h->peer.ready) return;
+  unsigned e = 0;
+  CHASE_CUDA(cudaMemcpyAsync(&e, h->peer.err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
+  CHASE_CUDA(cudaStreamSynchronize(h->stream));
+  if (e) {
+    h->peer.failed = true;
+    throw NcclError("fused peer all-reduce timed out (a peer stopped arriving)");
+  }
+}
+
+void peer_release(chase_handle* h) {
+  for (void* p : h->peer.opened) cudaIpcCloseMemHandle(p);
+  h->peer.opened.clear();
+  h->peer.stage.release();
+  h->peer.ctr.release();
+  h->peer.ready = false;
+}
+
+}  // namespace chase

@@ -104,17 +104,23 @@ static void launch3m(const ZgemmDesc& d, cudaStream_t st) {
   p.a_chunked = chunked ? 1 : 0;
   p.upper_only = d.upper_only ? 1 : 0;
   p.b_upper = d.b_upper ? 1 : 0;
+  if (d.red) {
+    if (d.upper_only) throw CudaError("fused all-reduce cannot skip tiles (upper_only)");
+    p.red = *d.red;
+  }
   const int grid = ceil_div(d.M, CFG::BM) * ceil_div(d.N, CFG::BN);
   zgemm3m_dmma_kernel<CFG, CONJ><<<grid, CFG::THREADS, CFG::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();
 }
+
+int zgemm3m_tiles(int M, int N) { return ceil_div(M, Z3Default::BM) * ceil_div(N, Z3Default::BN); }
 
 void zgemm(const ZgemmDesc& d0, cudaStream_t st) {
   if (d0.M <= 0 || d0.N <= 0) return;
   if (d0.K <= 0) throw CudaError("zgemm: K must be > 0");
   ZgemmDesc d = d0;
   if (!d.S) d.shift_lo = d.shift_hi = 0;
-  if (d.use3m) {
+  if (d.use3m || d.red) {
     if (d.conjA) launch3m<Z3Default, true>(d, st); else launch3m<Z3Default, false>(d, st);
     return;
   }

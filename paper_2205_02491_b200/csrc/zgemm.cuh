@@ -19,6 +19,7 @@
 #pragma once
 #include "common.cuh"
 #include "tma.cuh"
+#include "zgemm.h"
 
 namespace chase {
 
@@ -35,6 +36,7 @@ struct ZgemmParams {
   int a_chunked;        // forward A loaded by one 3-D TMA box (M % 8 == 0) instead of BM/8 2-D boxes
   int upper_only;       // skip output tiles strictly below the diagonal
   int b_upper;          // B is upper triangular: k-loop stops at the tile's last column
+  PeerRed red;          // f1: fused all-reduce over peer memory (red.n <= 1: off)
 };
 
 namespace zg {

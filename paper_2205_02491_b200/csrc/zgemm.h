@@ -5,6 +5,21 @@
 
 namespace chase {
 
+// f1: in-kernel all-reduce of a fused step's output over peer memory (CUDA IPC over NVLink).
+// Every comm rank stages its partial tile, the last rank to arrive on a tile (system-scope atomic
+// counter owned by comm rank 0) sums the n partials in comm-rank order -- identical bits on every
+// rank -- and stores the sum into every rank's replica, then bumps every rank's `done` counter.
+constexpr int kMaxPeers = 8;
+struct PeerRed {
+  int n = 0;                           // communicator size (<= 1: no fused reduction)
+  int me = 0;                          // my rank in the communicator
+  int64_t off = 0;                     // element offset of C inside the replica / staging buffers
+  double2* stage[kMaxPeers] = {};      // staging buffer base of every comm rank (same layout as C)
+  double2* out[kMaxPeers] = {};        // replica base of every comm rank (C = out[me] + off)
+  unsigned* ctr = nullptr;             // tile arrival counters (comm rank 0's memory)
+  unsigned* done[kMaxPeers] = {};      // completion counter of every comm rank
+};
+
 struct ZgemmDesc {
   int M = 0, N = 0, K = 0;
   bool conjA = false;            // op(A) = A^H with A stored K x M
@@ -17,10 +32,13 @@ struct ZgemmDesc {
   bool use3m = false;            // 3M (Gauss) complex product: 3 real DMMAs per complex MAC
   bool upper_only = false;       // only tiles on/above the diagonal are computed (Hermitian C)
   bool b_upper = false;          // B upper triangular (zeros below the diagonal are skipped)
+  const PeerRed* red = nullptr;  // f1: fused all-reduce of C over a communicator (3M kernel only)
 };
 
 // C = alpha*op(A)*B - alpha*gamma*S[shift rows] + beta*C   (all complex double, column-major)
 void zgemm(const ZgemmDesc& d, cudaStream_t st);
+// number of CTA tiles (= fused-reduction tiles) of the 3M kernel for an M x N output
+int zgemm3m_tiles(int M, int N);
 // The same contract for real double (op(A) = A^T when conjA; use3m ignored).  Real-symmetric f2.
 void dgemm(const ZgemmDesc& d, cudaStream_t st);
 

@@ -155,6 +155,9 @@ __global__ void __launch_bounds__(CFG::THREADS, 1)
   }
 
   const double ag = p.alpha * p.gamma;
+  const bool fused = p.red.n > 1;
+  // without f1 the result goes to C; with f1 this rank's partial goes to its staging buffer
+  double2* dst = fused ? p.red.stage[p.red.me] + p.red.off : p.C;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
     const int m = m0 + wm * 32 + mt * 8 + g;
@@ -175,16 +178,52 @@ __global__ void __launch_bounds__(CFG::THREADS, 1)
           vr -= ag * sv.x;
           vi -= ag * sv.y;
         }
-        double2* cp = p.C + (int64_t)m + (int64_t)n * p.ldc;
+        const int64_t o = (int64_t)m + (int64_t)n * p.ldc;
         if (p.beta != 0.0) {
-          const double2 cv = *cp;
+          const double2 cv = p.C[o];
           vr += p.beta * cv.x;
           vi += p.beta * cv.y;
         }
-        *cp = make_double2(vr, vi);
+        dst[o] = make_double2(vr, vi);
       }
     }
   }
+  if (!fused) return;
+  // ---- f1: arrive on this tile's counter; the last of the n ranks reduces and broadcasts
+  __shared__ int s_last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned old = atomicAdd_system(p.red.ctr + blockIdx.x, 1u);
+    s_last = ((old + 1u) % (unsigned)p.red.n) == 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence_system();
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int m = m0 + wm * 32 + mt * 8 + g;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = n0 + wn * 16 + nt * 8 + 2 * t + j;
+        if (n >= p.N) continue;
+        const int64_t o = p.red.off + (int64_t)m + (int64_t)n * p.ldc;
+        double2 acc = __ldcg(p.red.stage[0] + o);                  // comm-rank order: same bits everywhere
+        for (int r = 1; r < p.red.n; ++r) {
+          const double2 v = __ldcg(p.red.stage[r] + o);
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        for (int r = 0; r < p.red.n; ++r) p.red.out[r][o] = acc;
+      }
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < p.red.n) atomicAdd_system(p.red.done[threadIdx.x], 1u);
 }
 
 }  // namespace chase
