@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chase", choices=["chase", "reference"])
-    ap.add_argument("--n", type=int, default=N1, help="matrix order on 1 GPU (weak-scaled for more)")
+    ap.add_argument("--order", dest="n", type=int, default=N1, help="matrix order N on 1 GPU (weak-scaled for more)")
     ap.add_argument("--nev", type=int, default=NEV)
     ap.add_argument("--nex", type=int, default=NEX)
     ap.add_argument("--family", default="uniform")
@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c64", action="store_true", help="skip the complex-single filter sub-measurement")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: N = n sqrt(G) (paper P:717-718, default); strong: N = n on every G (config 3)")
     return ap.parse_args()
 
 
@@ -147,7 +149,7 @@ def run_reference(args, out):
         return 0
     world = args.gpus
     from paper_2205_02491_b200.dist import weak_scaled_n, grid_shape
-    N = weak_scaled_n(args.n, world)
+    N = weak_scaled_n(args.n, world) if args.scaling == "weak" else args.n
     per = max(3.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_sample(N, seconds=per / 3, family=args.family)
@@ -161,7 +163,7 @@ def run_reference(args, out):
     r, c = grid_shape(world)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded G2 generator, Table 1 spectrum)",
             "config": {"workload": f"config2 (weak-scaled): N={N} complex double {args.family}, nev={args.nev}, nex={args.nex}, deg={DEG}; oracle filter-step sample",
                        "N": N, "grid": f"{r}x{c}"},
@@ -203,7 +205,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     grid = grid_shape(world)
-    N = weak_scaled_n(args.n, world)
+    N = weak_scaled_n(args.n, world) if args.scaling == "weak" else args.n
     nev, nex = args.nev, args.nex
     row0, p, col0, q = shard(N, grid, rank)
 
@@ -343,9 +345,12 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": dev_s_max / args.steps * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-                "data": "synthetic (seeded G2 generator: H = Phi P C P^H Phi^H with the Table 1 Uniform spectrum, d_max=1, eps=1e-4)",
-                "config": {"workload": f"config2{' (weak-scaled)' if world > 1 else ''}: N={N} complex double {args.family}, nev={nev}, nex={nex}, deg={DEG}, one subspace iteration (P:727-731)",
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "c128",
+                "data": f"synthetic (seeded G2 generator: H = Phi P C P^H Phi^H with the Table 1 {args.family} spectrum, d_max=1, eps=1e-4)",
+                "config": {"workload": ({(N1, NEV, NEX): "config2", (60000, 1000, 300): "config3",
+                                         (115000, 1200, 400): "config4"}.get((args.n, nev, nex), "custom")
+                                        + (" (weak-scaled)" if world > 1 and args.scaling == "weak" else ""))
+                           + f": N={N} complex double {args.family}, nev={nev}, nex={nex}, deg={DEG}, one subspace iteration (P:727-731)",
                            "N": N, "nev": nev, "nex": nex, "deg": DEG, "grid": f"{grid[0]}x{grid[1]}",
                            "l2": "inputs larger than L2 (H shard %.1f GB >> 126 MB)" % (16e-9 * p * q)},
                 "wall_ms_per_step": t_wall / args.steps * 1e3,
