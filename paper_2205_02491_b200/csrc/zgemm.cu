@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Host launcher for the TMA + DMMA complex GEMM (zgemm.cuh) and the tensor-map encoder.
 #include "zgemm.h"
 #include "zgemm.cuh"
@@ -108,6 +109,8 @@ static void launch3m(const ZgemmDesc& d, cudaStream_t st) {
     if (d.upper_only) throw CudaError("fused all-reduce cannot skip tiles (upper_only)");
     p.red = *d.red;
   }
+  static const int group_m = std::getenv("CHASE_ZGEMM_GROUP_M") ? std::atoi(std::getenv("CHASE_ZGEMM_GROUP_M")) : 0;
+  p.group_m = group_m;
   const int grid = ceil_div(d.M, CFG::BM) * ceil_div(d.N, CFG::BN);
   zgemm3m_dmma_kernel<CFG, CONJ><<<grid, CFG::THREADS, CFG::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();

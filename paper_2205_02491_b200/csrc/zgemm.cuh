@@ -37,6 +37,7 @@ struct ZgemmParams {
   int upper_only;       // skip output tiles strictly below the diagonal
   int b_upper;          // B is upper triangular: k-loop stops at the tile's last column
   PeerRed red;          // f1: fused all-reduce over peer memory (red.n <= 1: off)
+  int group_m;          // 3M kernel tile rasterisation: M tiles per group (0: default 12)
 };
 
 namespace zg {

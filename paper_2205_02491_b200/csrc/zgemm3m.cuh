@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(CFG::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = (p.N + BN - 1) / BN;
   const int tiles_m = (p.M + BM - 1) / BM;
-  constexpr int GROUP_M = 12;
+  const int GROUP_M = p.group_m > 0 ? p.group_m : 12;
   const int per_group = GROUP_M * tiles_n;
   const int group = blockIdx.x / per_group;
   const int first_m = group * GROUP_M;
