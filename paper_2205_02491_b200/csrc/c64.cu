@@ -119,7 +119,7 @@ struct WFmt {        // W-layout block: 4 complex64 arrays, ld = p
 // one local fused step (no communication); `first` columns offset already applied by the caller
 template <int BN>
 void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const void* Hlo, const VFmt& v,
-                 const WFmt& w, int ncols, double alpha, double beta, double gamma, bool beta_on) {
+                 const WFmt& w, int ncols, double alpha, double beta, double gamma, bool beta_on, const C64Red* red) {
   using namespace tc;
   constexpr size_t SMEM = Cfg<BN>::SMEM;
   const Grid& g = h->grid;
@@ -129,8 +129,6 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   P.N = ncols;
   P.alpha = (float)alpha; P.beta = (float)beta; P.gamma = (float)gamma;
   P.beta_on = beta_on ? 1 : 0;
-  static const int lolo = getenv("CHASE_C64_LOLO") ? atoi(getenv("CHASE_C64_LOLO")) : 0;
-  P.lolo = lolo;
   static const int kcs = getenv("CHASE_C64_KC") ? atoi(getenv("CHASE_C64_KC")) : 0;
   P.kc_stages = kcs;
   if (dir == 0) {       // forward: W = alpha (H V - gamma E V) + beta W
@@ -169,17 +167,24 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   static bool attr[2] = {false, false};
   // CTA pairs (default; CHASE_C64_PAIR=0 selects the single-CTA kernel)
   static const bool pair = !getenv("CHASE_C64_PAIR") || atoi(getenv("CHASE_C64_PAIR")) != 0;
+  if (red && !pair) throw UsageError("fused c64 all-reduce needs the CTA-pair kernel");
+  if (red) P.red = *red;
   if (pair) {
     // CTA pairs: one cluster of 2 per 256-row x BN tile
     constexpr size_t SMEM2 = Cfg2<BN>::SMEM;
-    static bool attr2[2] = {false, false};
+    static bool attr2[4] = {false, false, false, false};
     const int grid2 = 2 * ceil_div(P.M, 2 * BMR) * ceil_div(P.N, BN);
+    auto go = [&](auto kern, int slot) {
+      if (!attr2[slot]) {
+        CHASE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
+        attr2[slot] = true;
+      }
+      kern<<<grid2, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
+    };
     if (dir == 0) {
-      if (!attr2[0]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel2<true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2)); attr2[0] = true; }
-      c64_step_kernel2<true, BN><<<grid2, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
+      if (red) go(c64_step_kernel2<true, BN, true>, 0); else go(c64_step_kernel2<true, BN, false>, 1);
     } else {
-      if (!attr2[1]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel2<false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2)); attr2[1] = true; }
-      c64_step_kernel2<false, BN><<<grid2, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
+      if (red) go(c64_step_kernel2<false, BN, true>, 2); else go(c64_step_kernel2<false, BN, false>, 3);
     }
     CHASE_CHECK_LAUNCH();
     return;
@@ -195,14 +200,26 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   CHASE_CHECK_LAUNCH();
 }
 
-// column tile: 128 (MMA N = 256, 2-stage ring) unless CHASE_C64_BN=64 (N = 128, 3 stages)
+// column tile: 128 (MMA N = 256) unless CHASE_C64_BN=64 (N = 128)
 void c64_step_local(chase_handle* h, int dir, const void* H, int64_t ldh, const void* Hlo, const VFmt& v,
-                    const WFmt& w, int ncols, double alpha, double beta, double gamma, bool beta_on) {
+                    const WFmt& w, int ncols, double alpha, double beta, double gamma, bool beta_on,
+                    const C64Red* red = nullptr) {
   static const int bn = [] { const char* e = getenv("CHASE_C64_BN"); return e ? atoi(e) : 128; }();
   if (bn == 64)
-    c64_step_bn<64>(h, dir, H, ldh, Hlo, v, w, ncols, alpha, beta, gamma, beta_on);
+    c64_step_bn<64>(h, dir, H, ldh, Hlo, v, w, ncols, alpha, beta, gamma, beta_on, red);
   else
-    c64_step_bn<128>(h, dir, H, ldh, Hlo, v, w, ncols, alpha, beta, gamma, beta_on);
+    c64_step_bn<128>(h, dir, H, ldh, Hlo, v, w, ncols, alpha, beta, gamma, beta_on, red);
+}
+
+// number of CTAs (= reduction tiles) the step launches
+int c64_step_tiles(int M, int N) {
+  static const int bn = [] { const char* e = getenv("CHASE_C64_BN"); return e ? atoi(e) : 128; }();
+  return 2 * ceil_div(M, 2 * tc::BMR) * ceil_div(N, bn == 64 ? 64 : 128);
+}
+
+static bool c64_pair_kernel() {
+  static const bool pair = !getenv("CHASE_C64_PAIR") || atoi(getenv("CHASE_C64_PAIR")) != 0;
+  return pair;
 }
 
 }  // namespace
@@ -382,6 +399,10 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
   const double sigma1 = e / (mu_1 - c);
   double sigma_prev = sigma1;
   int first = 0;
+  // f1: all-reduce inside the step kernel over peer memory (CTA-pair kernel only)
+  wfmt(h, ncap, 0);
+  const bool fused = (g.r > 1 || g.c > 1) && c64_pair_kernel() && peer_c64_ready(h);
+  const int64_t plane = 2 * std::max(p, q) * (int64_t)ncap;
   for (int k = 1; k <= kmax; ++k) {
     while (first < ncols && degrees[first] < k) ++first;
     double alpha, beta;
@@ -397,6 +418,38 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
     const int nk = ncols - first;
     VFmt v = vfmt(h, ncap, first);
     WFmt w = wfmt(h, ncap, first);
+    const int cn = (k & 1) ? g.c : g.r;
+    if (fused && cn > 1) {
+      const PeerRed& pr = (k & 1) ? h->peer.row : h->peer.col;
+      C64Red R;
+      R.n = pr.n;
+      R.me = pr.me;
+      R.ctr = pr.ctr;
+      float* own = (k & 1) ? h->c64w.as<float>() : h->c64v.as<float>();
+      for (int r = 0; r < pr.n; ++r) {
+        R.stage[r] = reinterpret_cast<float*>(pr.stage[r]);
+        R.base[r] = (k & 1) ? h->peer.c64w_row[r] : h->peer.c64v_col[r];
+        R.done[r] = pr.done[r];
+      }
+      if (k & 1) {
+        R.o0 = reinterpret_cast<float*>(w.w) - own;
+        R.o1 = reinterpret_cast<float*>(w.wr) - own;
+        R.o0lo = reinterpret_cast<float*>(w.wl) - own;
+        R.o1lo = reinterpret_cast<float*>(w.wrl) - own;
+      } else {
+        R.o0 = v.r - own;
+        R.o1 = v.i - own;
+        R.o0lo = v.rl - own;
+        R.o1lo = v.il - own;
+      }
+      R.plane = plane;
+      if (k & 1)
+        c64_step_local(h, 0, H, ldh, Hlo, v, w, nk, alpha * hs, beta, c * hs, g.beta_owner_fwd() && beta != 0.0, &R);
+      else
+        c64_step_local(h, 1, H, ldh, Hlo, v, w, nk, alpha * hs, beta, c * hs, g.beta_owner_bwd() && beta != 0.0, &R);
+      peer_wait(h, c64_step_tiles((k & 1) ? (int)(2 * p) : (int)q, nk));
+      continue;
+    }
     if (k & 1) {
       c64_step_local(h, 0, H, ldh, Hlo, v, w, nk, alpha * hs, beta, c * hs, g.beta_owner_fwd() && beta != 0.0);
       if (g.c > 1 && h->rowc) {
@@ -420,6 +473,7 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
       }
     }
   }
+  if (fused) peer_check(h);
   // columns of degree 0 were never touched: write back only the filtered suffix
   int f0 = 0;
   while (f0 < ncols && degrees[f0] == 0) ++f0;

@@ -26,8 +26,22 @@
 #include <cstdint>
 #include "common.cuh"
 #include "tma.cuh"
+#include "zgemm.h"
 
 namespace chase {
+
+// f1 for complex single: the same last-arriver tile reduction as the complex-double GEMM
+// (zgemm.h PeerRed), here on fp32 staging; the reducer also writes the derived operand formats
+// (rotated / lo copies) into every replica.
+struct C64Red {
+  int n = 0, me = 0;
+  float* stage[kMaxPeers] = {};    // staging buffer of every comm rank
+  float* base[kMaxPeers] = {};     // operand-format buffer of every comm rank (c64w fwd / c64v bwd)
+  int64_t o0 = 0, o1 = 0, o0lo = 0, o1lo = 0;   // offsets (floats) of Y0 / Y1 / Y0lo / Y1lo from base
+  int64_t plane = 0;               // staging offset (floats) of the backward's Im plane
+  unsigned* ctr = nullptr;
+  unsigned* done[kMaxPeers] = {};
+};
 
 struct C64Params {
   int M, N, K;             // output rows (complex: fwd counts real rows 2*M_complex), cols, k (real MMA k)
@@ -44,8 +58,8 @@ struct C64Params {
   float* Y1lo;
   int64_t ldy;              // in floats (fwd: 2*p rows; bwd: q)
   int beta_on;
-  int lolo;                 // diagnostic: also issue the A_lo B_lo MMA (4xTF32)
   int kc_stages;            // K chunk (in BK stages) per fresh TMEM accumulator; 0 = default
+  C64Red red;               // f1 (pair kernel): fused all-reduce over peer memory when red.n > 1
 };
 
 namespace tc {
@@ -100,6 +114,106 @@ __device__ __forceinline__ float tf32_lo(float x) {
   return tf32_rn(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
 }
 }  // namespace tc
+
+// f1 epilogue (pair kernel, 8 drain warps = 256 threads, named barrier 1): stage this rank's
+// partial, arrive on the tile counter, and if last sum the partials in comm-rank order and write
+// every replica's operand formats.
+__device__ __forceinline__ void drain_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <bool FWD, int HN>
+__device__ __forceinline__ void c64_epilogue_fused(const C64Params& p, int row, int nbase, const float (&a1)[HN],
+                                                   const float (&a2)[HN]) {
+  const C64Red& R = p.red;
+  const float ag = p.alpha * p.gamma;
+  float* st = R.stage[R.me];
+  const bool odd = (row & 1);
+#pragma unroll
+  for (int j = 0; j < HN; ++j) {
+    const int n = nbase + j;
+    const bool ok = n < p.N && row < p.M;
+    const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
+    if constexpr (FWD) {
+      const float d2p = __shfl_xor_sync(0xffffffffu, a2[j], 1);
+      float v = (odd ? (a1[j] + d2p) : (a1[j] - d2p)) * p.alpha;
+      const int mc = row >> 1;
+      if (ok) {
+        if (mc >= p.shift_lo && mc < p.shift_hi) {
+          const float* src = odd ? p.S1 : p.S0;
+          v -= ag * src[(int64_t)mc + p.shift_off + (int64_t)n * p.lds];
+        }
+        if (p.beta_on) v += p.beta * p.Y0[o];
+        st[o] = v;
+      }
+    } else {
+      if (ok) {
+        float vr = p.alpha * a1[j], vi = p.alpha * a2[j];
+        if (row >= p.shift_lo && row < p.shift_hi) {
+          const float* src = p.S0 + 2 * ((int64_t)row + p.shift_off) + 2 * (int64_t)n * p.lds;
+          vr -= ag * src[0];
+          vi -= ag * src[1];
+        }
+        if (p.beta_on) {
+          vr += p.beta * p.Y0[o];
+          vi += p.beta * p.Y1[o];
+        }
+        st[o] = vr;
+        st[R.plane + o] = vi;
+      }
+    }
+  }
+  __shared__ int s_last;
+  __threadfence_system();
+  drain_bar();
+  if (threadIdx.x == 64) {
+    const unsigned old = atomicAdd_system(R.ctr + blockIdx.x, 1u);
+    s_last = ((old + 1u) % (unsigned)R.n) == 0u;
+  }
+  drain_bar();
+  if (!s_last) return;
+  __threadfence_system();
+#pragma unroll 4
+  for (int j = 0; j < HN; ++j) {
+    const int n = nbase + j;
+    const bool ok = n < p.N && row < p.M;
+    const int64_t o = (int64_t)row + (int64_t)n * p.ldy;
+    if constexpr (FWD) {
+      float v = 0.f;
+      if (ok) {
+        v = __ldcg(R.stage[0] + o);
+        for (int r = 1; r < R.n; ++r) v += __ldcg(R.stage[r] + o);
+      }
+      const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
+      if (ok) {
+        const float rot = odd ? -vp : vp;
+        const float vl = tc::tf32_lo(v), rl = tc::tf32_lo(rot);
+        for (int r = 0; r < R.n; ++r) {
+          float* b = R.base[r];
+          b[R.o0 + o] = v;
+          b[R.o1 + o] = rot;
+          b[R.o0lo + o] = vl;
+          b[R.o1lo + o] = rl;
+        }
+      }
+    } else if (ok) {
+      float vr = __ldcg(R.stage[0] + o), vi = __ldcg(R.stage[0] + R.plane + o);
+      for (int r = 1; r < R.n; ++r) {
+        vr += __ldcg(R.stage[r] + o);
+        vi += __ldcg(R.stage[r] + R.plane + o);
+      }
+      const float vrl = tc::tf32_lo(vr), vil = tc::tf32_lo(vi);
+      for (int r = 0; r < R.n; ++r) {
+        float* b = R.base[r];
+        b[R.o0 + o] = vr;
+        b[R.o1 + o] = vi;
+        b[R.o0lo + o] = vrl;
+        b[R.o1lo + o] = vil;
+      }
+    }
+  }
+  __threadfence_system();
+  drain_bar();
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + R.n) atomicAdd_system(R.done[threadIdx.x - 64], 1u);
+}
 
 // fused epilogue from the drained FP32 accumulators of one thread (one row, HN columns of each of
 // D1 / D2): shift on the intersection rows, scale, beta term, and the next step's operand formats
@@ -282,7 +396,6 @@ __global__ void __launch_bounds__(C64_THREADS, 1)
           tc::mma_tf32(td, da, db, idesc, acc);             // D = A_hi B_hi
           tc::mma_tf32(td, da, dbl, idesc, 1u);             //   + A_hi B_lo
           tc::mma_tf32(td, dal, db, idesc, 1u);             //   + A_lo B_hi
-          if (p.lolo) tc::mma_tf32(td, dal, dbl, idesc, 1u);  //   + A_lo B_lo (diagnostic)
         }
         tc::commit(empty + s);                              // smem slot free once these MMAs retire
         if ((kt % CH) == CH - 1 || kt == KT - 1) tc::commit(acc_full + b);
@@ -388,7 +501,7 @@ struct Cfg2 {
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
 };
 
-template <bool FWD, int BN>
+template <bool FWD, int BN, bool RED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
     c64_step_kernel2(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tAlo,
                      const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB1lo,
@@ -536,7 +649,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
       __syncwarp();
       if (lane == 0) tc2::arrive_cluster(tc2::mapa(smem_u32(acc_empty + b), 0));
     }
-    c64_epilogue<FWD, HN>(p, row, n0 + half * HN, a1, a2);
+    if constexpr (RED)
+      c64_epilogue_fused<FWD, HN>(p, row, n0 + half * HN, a1, a2);
+    else
+      c64_epilogue<FWD, HN>(p, row, n0 + half * HN, a1, a2);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   tc2::cluster_sync();

@@ -104,6 +104,9 @@ struct chase_handle {
     unsigned* err = nullptr;
     unsigned expected = 0;
     chase::PeerRed row, col;
+    bool c64_ready = false;
+    float* c64w_row[chase::kMaxPeers] = {};   // row peers' c64 W-layout format buffers
+    float* c64v_col[chase::kMaxPeers] = {};   // column peers' c64 V-layout format buffers
     std::vector<void*> opened;
   } peer;
 };
@@ -151,6 +154,7 @@ void c64_convert(void* dst, int64_t ldd, bool dst_c128, const void* src, int64_t
 
 // f1 (peer.cu): set up / use the fused peer all-reduce of the filter steps
 bool peer_reduce_ready(chase_handle* h);
+bool peer_c64_ready(chase_handle* h);
 const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y);
 void peer_wait(chase_handle* h, int tiles);
 void peer_check(chase_handle* h);

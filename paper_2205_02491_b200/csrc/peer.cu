@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <stdexcept>
 #include <vector>
 #include "handle.h"
 
@@ -62,9 +63,9 @@ void* open_peer(chase_handle* h, const cudaIpcMemHandle_t& hd) {
 }
 }  // namespace
 
-bool peer_reduce_ready(chase_handle* h) {
+static bool peer_base_ready(chase_handle* h) {
   const Grid& g = h->grid;
-  if (h->peer.failed || !h->opt.fused_reduce || h->dtype != CHASE_C128 || !h->opt.gemm3m) return false;
+  if (h->peer.failed || !h->opt.fused_reduce) return false;
   if (h->world_size <= 1 || !h->world || (g.r <= 1 && g.c <= 1)) return false;
   if (g.r > kMaxPeers || g.c > kMaxPeers) return false;
   if (h->peer.ready) return true;
@@ -119,6 +120,42 @@ bool peer_reduce_ready(chase_handle* h) {
   return true;
 }
 
+bool peer_reduce_ready(chase_handle* h) {
+  if (h->dtype == CHASE_R64 || !h->opt.gemm3m) return false;
+  return peer_base_ready(h);
+}
+
+// complex single: the replicas are the operand-format buffers c64w (row comm) / c64v (column
+// comm); their handles are exchanged once they exist (c64.cu allocates them on first use)
+bool peer_c64_ready(chase_handle* h) {
+  if (h->real() || !peer_base_ready(h)) return false;
+  if (h->peer.c64_ready) return true;
+  const Grid& g = h->grid;
+  if (!h->c64v.p || !h->c64w.p) throw std::logic_error("peer_c64_ready before the c64 formats exist");
+  struct H2 { cudaIpcMemHandle_t buf; } mine_r{}, mine_c{};
+  CHASE_CUDA(cudaIpcGetMemHandle(&mine_r.buf, h->c64w.p));
+  CHASE_CUDA(cudaIpcGetMemHandle(&mine_c.buf, h->c64v.p));
+  auto xchg = [&](ncclComm_t comm, int n, int me, const H2& mine, float** out, void* own) {
+    std::vector<H2> all(n);
+    void* d = nullptr;
+    CHASE_CUDA(cudaMalloc(&d, sizeof(H2) * (n + 1)));
+    CHASE_CUDA(cudaMemcpyAsync(d, &mine, sizeof(H2), cudaMemcpyHostToDevice, h->stream));
+    CHASE_NCCL(ncclAllGather(d, reinterpret_cast<char*>(d) + sizeof(H2), sizeof(H2), ncclUint8, comm, h->stream));
+    CHASE_CUDA(cudaMemcpyAsync(all.data(), reinterpret_cast<char*>(d) + sizeof(H2), sizeof(H2) * n,
+                               cudaMemcpyDeviceToHost, h->stream));
+    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    cudaFree(d);
+    for (int r = 0; r < n; ++r)
+      out[r] = r == me ? reinterpret_cast<float*>(own) : reinterpret_cast<float*>(open_peer(h, all[r].buf));
+  };
+  if (g.c > 1) xchg(h->rowc, g.c, g.j, mine_r, h->peer.c64w_row, h->c64w.p);
+  if (g.r > 1) xchg(h->colc, g.r, g.i, mine_c, h->peer.c64v_col, h->c64v.p);
+  h->peer.c64_ready = true;
+  if (std::getenv("CHASE_DEBUG_PEER"))
+    std::fprintf(stderr, "[chase] rank %d: fused peer all-reduce ready for complex single\n", g.rank);
+  return true;
+}
+
 // launch-side helpers for one fused step on the internal buffers: `Y` lies in h->W (dir 0) or h->V
 const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y) {
   PeerRed& pr = dir == 0 ? h->peer.row : h->peer.col;
@@ -151,6 +188,7 @@ void peer_release(chase_handle* h) {
   h->peer.stage.release();
   h->peer.ctr.release();
   h->peer.ready = false;
+  h->peer.c64_ready = false;
 }
 
 }  // namespace chase
