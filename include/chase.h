@@ -100,7 +100,11 @@ chase_status chase_init(chase_handle** out, const chase_init_args* args);
  * complex-single shadow of the shard -- the tcgen05 3xTF32 path, ~3.5x the FP64 filter rate --
  * while every active column's residual is above r, with degrees aimed at max(tol, 1e-5); later
  * iterations use the FP64 filter, so the returned pairs meet tol as usual.  Costs one extra
- * shard-sized buffer (the complex64 shadow and its 3xTF32 low part)). */
+ * shard-sized buffer (the complex64 shadow and its 3xTF32 low part)),
+ * fused_reduce=1 (on a grid the complex-double filter steps sum their partial products
+ * inside the GEMM epilogue over peer memory -- CUDA IPC over NVLink -- instead of ncclAllReduce),
+ * fused_reduce_c64=0 (the same for the complex-single filter; off by default: measured slower
+ * than ncclAllReduce + local format rebuild at N = 170000 on 2x2). */
 chase_status chase_set_option(chase_handle* h, const char* key, double value);
 
 /* This rank's shard: rows [row0, row0+p) and columns [col0, col0+q) of H. */

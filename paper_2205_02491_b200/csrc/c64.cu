@@ -401,7 +401,7 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
   int first = 0;
   // f1: all-reduce inside the step kernel over peer memory (CTA-pair kernel only)
   wfmt(h, ncap, 0);
-  const bool fused = (g.r > 1 || g.c > 1) && c64_pair_kernel() && peer_c64_ready(h);
+  const bool fused = (g.r > 1 || g.c > 1) && h->opt.fused_reduce_c64 && c64_pair_kernel() && peer_c64_ready(h);
   const int64_t plane = 2 * std::max(p, q) * (int64_t)ncap;
   for (int k = 1; k <= kmax; ++k) {
     while (first < ncols && degrees[first] < k) ++first;
@@ -448,6 +448,15 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
       else
         c64_step_local(h, 1, H, ldh, Hlo, v, w, nk, alpha * hs, beta, c * hs, g.beta_owner_bwd() && beta != 0.0, &R);
       peer_wait(h, c64_step_tiles((k & 1) ? (int)(2 * p) : (int)q, nk));
+      if (k & 1) {
+        k_to_wfmt<<<grid_for(p * nk), 256, 0, h->stream>>>(w.w, w.ld, p, nk, nullptr, w.wr, w.wl, w.wrl, w.ld);
+        CHASE_CHECK_LAUNCH();
+      } else {
+        k_lo<<<grid_for(q * nk), 256, 0, h->stream>>>(v.rl, v.r, q, nk, v.ld, v.ld);
+        CHASE_CHECK_LAUNCH();
+        k_lo<<<grid_for(q * nk), 256, 0, h->stream>>>(v.il, v.i, q, nk, v.ld, v.ld);
+        CHASE_CHECK_LAUNCH();
+      }
       continue;
     }
     if (k & 1) {

@@ -116,8 +116,9 @@ __device__ __forceinline__ float tf32_lo(float x) {
 }  // namespace tc
 
 // f1 epilogue (pair kernel, 8 drain warps = 256 threads, named barrier 1): stage this rank's
-// partial, arrive on the tile counter, and if last sum the partials in comm-rank order and write
-// every replica's operand formats.
+// partial, arrive on the tile counter, and if last sum the partials in comm-rank order and store
+// the sum into every replica (the rotated / lo copies are rebuilt locally after the step: one
+// remote array instead of four).
 __device__ __forceinline__ void drain_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <bool FWD, int HN>
@@ -183,30 +184,18 @@ __device__ __forceinline__ void c64_epilogue_fused(const C64Params& p, int row, 
         for (int r = 1; r < R.n; ++r) v += __ldcg(R.stage[r] + o);
       }
       const float vp = __shfl_xor_sync(0xffffffffu, v, 1);
-      if (ok) {
-        const float rot = odd ? -vp : vp;
-        const float vl = tc::tf32_lo(v), rl = tc::tf32_lo(rot);
-        for (int r = 0; r < R.n; ++r) {
-          float* b = R.base[r];
-          b[R.o0 + o] = v;
-          b[R.o1 + o] = rot;
-          b[R.o0lo + o] = vl;
-          b[R.o1lo + o] = rl;
-        }
-      }
+      (void)vp;
+      if (ok)
+        for (int r = 0; r < R.n; ++r) R.base[r][R.o0 + o] = v;   // derived formats: rebuilt locally
     } else if (ok) {
       float vr = __ldcg(R.stage[0] + o), vi = __ldcg(R.stage[0] + R.plane + o);
       for (int r = 1; r < R.n; ++r) {
         vr += __ldcg(R.stage[r] + o);
         vi += __ldcg(R.stage[r] + R.plane + o);
       }
-      const float vrl = tc::tf32_lo(vr), vil = tc::tf32_lo(vi);
       for (int r = 0; r < R.n; ++r) {
-        float* b = R.base[r];
-        b[R.o0 + o] = vr;
-        b[R.o1 + o] = vi;
-        b[R.o0lo + o] = vrl;
-        b[R.o1lo + o] = vil;
+        R.base[r][R.o0 + o] = vr;
+        R.base[r][R.o1 + o] = vi;
       }
     }
   }

@@ -428,6 +428,7 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     else if (k == "gemm3m") h->opt.gemm3m = v != 0.0;
     else if (k == "mixed_filter") h->opt.mixed_filter = v;
     else if (k == "fused_reduce") h->opt.fused_reduce = v != 0.0;
+    else if (k == "fused_reduce_c64") h->opt.fused_reduce_c64 = v != 0.0;
     else throw UsageError("unknown option " + k);
     return CHASE_OK;
   }, false);

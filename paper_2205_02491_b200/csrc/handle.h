@@ -61,6 +61,7 @@ struct Options {
   bool gemm3m = true;         // 3M complex products in the filter / HQ GEMMs
   double mixed_filter = 0.0;  // f4: complex-single filter while all active residuals exceed this
   bool fused_reduce = true;   // f1: filter steps all-reduce inside the GEMM over peer memory
+  bool fused_reduce_c64 = false;  // f1 for the complex-single filter (measured slower than NCCL + rebuild)
 };
 
 }  // namespace chase

@@ -17,11 +17,13 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("dtype", ["c128", "c64", "r64"])
+@pytest.mark.parametrize("dtype", ["c128", "c64", "c64-fused", "r64"])
 def test_two_gpu_grid(dtype):
     if _ngpu() < 2:
         pytest.skip("needs >= 2 GPUs")
-    env = dict(os.environ, MG_DTYPE=dtype, CHASE_DEBUG_PEER="1")
+    env = dict(os.environ, MG_DTYPE=dtype.split("-")[0], CHASE_DEBUG_PEER="1")
+    if dtype == "c64-fused":
+        env["MG_FUSED_C64"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "tools", "mgpu_check.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
@@ -31,3 +33,5 @@ def test_two_gpu_grid(dtype):
     assert res["ok"], res
     if dtype == "c128":       # the filter ran through the fused peer all-reduce (f1)
         assert "fused peer all-reduce ready" in r.stderr
+    if dtype == "c64-fused":
+        assert "fused peer all-reduce ready for complex single" in r.stderr

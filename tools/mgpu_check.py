@@ -44,6 +44,8 @@ def main():
     ch = pkg.Chase(N, 800 if single else nev, nex, grid=grid, rank=rank, world_size=world, nccl_id=nid, device=local,
                    dtype=dtype)
     assert ch.local_layout() == (r0, p, c0, q)
+    if os.environ.get("MG_FUSED_C64"):
+        ch.set_option("fused_reduce_c64", 1)
     dH = dev(cast(H[r0:r0 + p, c0:c0 + q]))
     ok = True
     out = []
