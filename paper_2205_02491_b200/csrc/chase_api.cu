@@ -171,7 +171,7 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       d.red = peer_red_for(h, dir, Yk);
       if (d.red) {
         gemm(h, d);
-        peer_wait(h, zgemm3m_tiles(d.M, d.N));
+        peer_wait(h, h->real() ? dgemm_tiles(d.M, d.N) : zgemm3m_tiles(d.M, d.N));
       } else {                                   // this direction's communicator has one rank
         gemm(h, d);
       }
@@ -472,11 +472,15 @@ chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, 
     order_after_user(h);
     const Grid& g = h->grid;
     // f1 runs on the library's V / W workspace (the peers' replicas): stage the caller's block
-    const bool staged = h->dtype == CHASE_C128 && h->opt.fused_reduce && h->opt.gemm3m && h->world_size > 1 &&
+    const bool staged = !h->c64() && h->opt.fused_reduce && (h->real() || h->opt.gemm3m) && h->world_size > 1 &&
                         (g.r > 1 || g.c > 1) && ncols > 0 && ncols <= h->n_e_max;
     int64_t mv;
     if (h->c64()) {
       mv = c64_filter(h, H, ldh, V, ldv, ncols, degrees, b_sup, mu_1, mu_ne);
+    } else if (staged && h->real()) {
+      copy2d<double>(h->V.p, q, V, ldv, q, ncols, h->stream);
+      mv = filter(h, H, ldh, h->V.p, q, h->W.p, p, ncols, degrees, b_sup, mu_1, mu_ne);
+      copy2d<double>(V, ldv, h->V.p, q, q, ncols, h->stream);
     } else if (staged) {
       copy2d<double2>(h->V.p, q, V, ldv, q, ncols, h->stream);
       mv = filter(h, H, ldh, h->V.p, q, h->W.p, p, ncols, degrees, b_sup, mu_1, mu_ne);

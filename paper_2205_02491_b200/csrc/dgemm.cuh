@@ -14,6 +14,7 @@
 #pragma once
 #include "common.cuh"
 #include "tma.cuh"
+#include "zgemm.h"
 #include "zgemm.cuh"
 
 namespace chase {
@@ -42,6 +43,7 @@ struct DgemmParams {
   int upper_only;
   int b_upper;
   int a_chunked;        // TMA path: forward A as one 3-D box (M % 16 == 0)
+  PeerRed red;          // f1: fused all-reduce over peer memory (buffers hold doubles; red.n <= 1: off)
 };
 
 namespace dg {
@@ -225,6 +227,8 @@ __global__ void __launch_bounds__(DCfg::THREADS, 1)
   if constexpr (!USE_TMA) dg::cp_wait<0>();
 
   const double ag = p.alpha * p.gamma;
+  const bool fused = p.red.n > 1;
+  double* dst = fused ? reinterpret_cast<double*>(p.red.stage[p.red.me]) + p.red.off : p.C;
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
     const int m = m0 + wm * 64 + mt * 8 + g;
@@ -238,12 +242,42 @@ __global__ void __launch_bounds__(DCfg::THREADS, 1)
         if (n >= p.N) continue;
         double v = p.alpha * acc[mt][nt][j];
         if (shifted) v -= ag * p.S[(int64_t)m + p.shift_off + (int64_t)n * p.lds];
-        double* cp = p.C + (int64_t)m + (int64_t)n * p.ldc;
-        if (p.beta != 0.0) v += p.beta * *cp;
-        *cp = v;
+        const int64_t o = (int64_t)m + (int64_t)n * p.ldc;
+        if (p.beta != 0.0) v += p.beta * p.C[o];
+        dst[o] = v;
       }
     }
   }
+  if (!fused) return;
+  // ---- f1 (see zgemm3m.cuh): last of the n ranks to arrive on this tile reduces and broadcasts
+  __shared__ int s_last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned old = atomicAdd_system(p.red.ctr + blockIdx.x, 1u);
+    s_last = ((old + 1u) % (unsigned)p.red.n) == 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence_system();
+#pragma unroll 2
+  for (int mt = 0; mt < 8; ++mt) {
+    const int m = m0 + wm * 64 + mt * 8 + g;
+    if (m >= p.M) continue;
+    for (int nt = 0; nt < 4; ++nt) {
+      for (int j = 0; j < 2; ++j) {
+        const int n = n0 + wn * 32 + nt * 8 + 2 * t + j;
+        if (n >= p.N) continue;
+        const int64_t o = p.red.off + (int64_t)m + (int64_t)n * p.ldc;
+        double a = __ldcg(reinterpret_cast<const double*>(p.red.stage[0]) + o);
+        for (int r = 1; r < p.red.n; ++r) a += __ldcg(reinterpret_cast<const double*>(p.red.stage[r]) + o);
+        for (int r = 0; r < p.red.n; ++r) reinterpret_cast<double*>(p.red.out[r])[o] = a;
+      }
+    }
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < p.red.n) atomicAdd_system(p.red.done[threadIdx.x], 1u);
 }
 
 }  // namespace chase

@@ -100,7 +100,7 @@ struct chase_handle {
   // f1: fused all-reduce over peer memory (peer.cu)
   struct Peer {
     bool ready = false, failed = false;
-    chase::DBuf stage, ctr;
+    chase::DBuf stage, ctr, flag;
     unsigned* done_local = nullptr;
     unsigned* err = nullptr;
     unsigned expected = 0;

@@ -63,29 +63,61 @@ void* open_peer(chase_handle* h, const cudaIpcMemHandle_t& hd) {
 }
 }  // namespace
 
+// every rank's local success flag, min over the world (collective); false if any rank failed
+static bool all_ok(chase_handle* h, bool ok) {
+  h->peer.flag.alloc(sizeof(int));
+  int v = ok ? 1 : 0;
+  CHASE_CUDA(cudaMemcpyAsync(h->peer.flag.p, &v, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+  CHASE_NCCL(ncclAllReduce(h->peer.flag.p, h->peer.flag.p, 1, ncclInt32, ncclMin, h->world, h->stream));
+  CHASE_CUDA(cudaMemcpyAsync(&v, h->peer.flag.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CHASE_CUDA(cudaStreamSynchronize(h->stream));
+  return v != 0;
+}
+
+static void give_up(chase_handle* h, const char* why) {
+  for (void* p : h->peer.opened) cudaIpcCloseMemHandle(p);
+  h->peer.opened.clear();
+  h->peer.failed = true;
+  if (std::getenv("CHASE_DEBUG_PEER"))
+    std::fprintf(stderr, "[chase] rank %d: fused peer all-reduce unavailable (%s); using NCCL\n", h->grid.rank, why);
+}
+
 static bool peer_base_ready(chase_handle* h) {
   const Grid& g = h->grid;
   if (h->peer.failed || !h->opt.fused_reduce) return false;
   if (h->world_size <= 1 || !h->world || (g.r <= 1 && g.c <= 1)) return false;
   if (g.r > kMaxPeers || g.c > kMaxPeers) return false;
   if (h->peer.ready) return true;
-  // ---- collective setup (every rank of the grid reaches this point with the same options)
+  // ---- collective setup (every rank of the grid reaches this point with the same options).  Local
+  // failures (no IPC / peer access in this environment, allocation) are agreed on over the world,
+  // so either every rank uses the fused path or none does.
   const int64_t p = g.rows.len, q = g.cols.len, ne = h->n_e_max;
-  h->peer.stage.alloc(16 * (size_t)std::max(p, q) * ne);
-  h->peer.ctr.alloc(sizeof(unsigned) * (2 * (size_t)kCtrPerComm + 64));
-  CHASE_CUDA(cudaMemsetAsync(h->peer.ctr.p, 0, h->peer.ctr.bytes, h->stream));
-  unsigned* base = h->peer.ctr.as<unsigned>();
-  h->peer.done_local = base + 2 * kCtrPerComm;
-  h->peer.err = base + 2 * kCtrPerComm + 32;
+  bool ok = true;
   Handles row_mine{}, col_mine{};
-  CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.stage, h->peer.stage.p));
-  CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.ctr, h->peer.ctr.p));
-  col_mine = row_mine;
-  CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.vec, h->W.p));      // row comm sums W-layout blocks
-  CHASE_CUDA(cudaIpcGetMemHandle(&col_mine.vec, h->V.p));      // column comm sums V-layout blocks
+  unsigned* base = nullptr;
+  try {
+    h->peer.stage.alloc(16 * (size_t)std::max(p, q) * ne);
+    h->peer.ctr.alloc(sizeof(unsigned) * (2 * (size_t)kCtrPerComm + 64));
+    CHASE_CUDA(cudaMemsetAsync(h->peer.ctr.p, 0, h->peer.ctr.bytes, h->stream));
+    base = h->peer.ctr.as<unsigned>();
+    h->peer.done_local = base + 2 * kCtrPerComm;
+    h->peer.err = base + 2 * kCtrPerComm + 32;
+    CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.stage, h->peer.stage.p));
+    CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.ctr, h->peer.ctr.p));
+    col_mine = row_mine;
+    CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.vec, h->W.p));      // row comm sums W-layout blocks
+    CHASE_CUDA(cudaIpcGetMemHandle(&col_mine.vec, h->V.p));      // column comm sums V-layout blocks
+  } catch (const std::exception&) {
+    cudaGetLastError();
+    ok = false;
+  }
   std::vector<Handles> rows_h, cols_h;
   if (g.c > 1) gather_handles(h, h->rowc, g.c, row_mine, rows_h);
   if (g.r > 1) gather_handles(h, h->colc, g.r, col_mine, cols_h);
+  if (!all_ok(h, ok)) {
+    give_up(h, "setup");
+    return false;
+  }
   auto fill = [&](PeerRed& pr, int n, int me, const std::vector<Handles>& hs, void* own_vec, int ctr_slot) {
     pr.n = n;
     pr.me = me;
@@ -105,13 +137,20 @@ static bool peer_base_ready(chase_handle* h) {
     pr.ctr = ctrs[0] + (size_t)ctr_slot * kCtrPerComm;        // owned by comm rank 0
   };
   // rank within the row comm = j (split key j), within the column comm = i (key i)
-  if (g.c > 1) fill(h->peer.row, g.c, g.j, rows_h, h->W.p, 0);
-  if (g.r > 1) fill(h->peer.col, g.r, g.i, cols_h, h->V.p, 1);
-  CHASE_CUDA(cudaStreamSynchronize(h->stream));
-  // barrier over the world (sum of the zeroed error words): every rank's counters are zeroed before
-  // anyone may arrive on them
-  CHASE_NCCL(ncclAllReduce(h->peer.err, h->peer.err, 1, ncclUint32, ncclSum, h->world, h->stream));
-  CHASE_CUDA(cudaStreamSynchronize(h->stream));
+  try {
+    if (g.c > 1) fill(h->peer.row, g.c, g.j, rows_h, h->W.p, 0);
+    if (g.r > 1) fill(h->peer.col, g.r, g.i, cols_h, h->V.p, 1);
+    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+  } catch (const std::exception&) {
+    cudaGetLastError();
+    ok = false;
+  }
+  if (!all_ok(h, ok)) {                  // also the barrier: every rank's counters are zeroed
+    h->peer.row = PeerRed{};
+    h->peer.col = PeerRed{};
+    give_up(h, "opening peer memory");
+    return false;
+  }
   h->peer.expected = 0;
   h->peer.ready = true;
   if (std::getenv("CHASE_DEBUG_PEER"))
@@ -121,7 +160,7 @@ static bool peer_base_ready(chase_handle* h) {
 }
 
 bool peer_reduce_ready(chase_handle* h) {
-  if (h->dtype == CHASE_R64 || !h->opt.gemm3m) return false;
+  if (h->dtype == CHASE_C128 && !h->opt.gemm3m) return false;     // the 4M kernel has no fused epilogue
   return peer_base_ready(h);
 }
 
@@ -135,6 +174,7 @@ bool peer_c64_ready(chase_handle* h) {
   struct H2 { cudaIpcMemHandle_t buf; } mine_r{}, mine_c{};
   CHASE_CUDA(cudaIpcGetMemHandle(&mine_r.buf, h->c64w.p));
   CHASE_CUDA(cudaIpcGetMemHandle(&mine_c.buf, h->c64v.p));
+  bool ok = true;
   auto xchg = [&](ncclComm_t comm, int n, int me, const H2& mine, float** out, void* own) {
     std::vector<H2> all(n);
     void* d = nullptr;
@@ -145,11 +185,20 @@ bool peer_c64_ready(chase_handle* h) {
                                cudaMemcpyDeviceToHost, h->stream));
     CHASE_CUDA(cudaStreamSynchronize(h->stream));
     cudaFree(d);
-    for (int r = 0; r < n; ++r)
-      out[r] = r == me ? reinterpret_cast<float*>(own) : reinterpret_cast<float*>(open_peer(h, all[r].buf));
+    try {
+      for (int r = 0; r < n; ++r)
+        out[r] = r == me ? reinterpret_cast<float*>(own) : reinterpret_cast<float*>(open_peer(h, all[r].buf));
+    } catch (const std::exception&) {
+      cudaGetLastError();
+      ok = false;
+    }
   };
   if (g.c > 1) xchg(h->rowc, g.c, g.j, mine_r, h->peer.c64w_row, h->c64w.p);
   if (g.r > 1) xchg(h->colc, g.r, g.i, mine_c, h->peer.c64v_col, h->c64v.p);
+  if (!all_ok(h, ok)) {
+    give_up(h, "opening complex-single peer buffers");
+    return false;
+  }
   h->peer.c64_ready = true;
   if (std::getenv("CHASE_DEBUG_PEER"))
     std::fprintf(stderr, "[chase] rank %d: fused peer all-reduce ready for complex single\n", g.rank);
@@ -161,7 +210,7 @@ const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y) {
   PeerRed& pr = dir == 0 ? h->peer.row : h->peer.col;
   if (pr.n <= 1) return nullptr;
   const char* base = reinterpret_cast<const char*>(dir == 0 ? h->W.p : h->V.p);
-  pr.off = (reinterpret_cast<const char*>(Y) - base) / 16;
+  pr.off = (reinterpret_cast<const char*>(Y) - base) / (h->real() ? 8 : 16);
   return &pr;
 }
 
@@ -187,6 +236,7 @@ void peer_release(chase_handle* h) {
   h->peer.opened.clear();
   h->peer.stage.release();
   h->peer.ctr.release();
+  h->peer.flag.release();
   h->peer.ready = false;
   h->peer.c64_ready = false;
 }

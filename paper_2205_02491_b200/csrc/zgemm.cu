@@ -303,10 +303,16 @@ static void launch_d(const ZgemmDesc& d, cudaStream_t st) {
   p.upper_only = d.upper_only ? 1 : 0;
   p.b_upper = d.b_upper ? 1 : 0;
   p.a_chunked = chunked ? 1 : 0;
+  if (d.red) {
+    if (d.upper_only) throw CudaError("fused all-reduce cannot skip tiles (upper_only)");
+    p.red = *d.red;
+  }
   const int grid = ceil_div(d.M, DCfg::BM) * ceil_div(d.N, DCfg::BN);
   dgemm_dmma_kernel<TRANS, TMA><<<grid, DCfg::THREADS, DCfg::SMEM, st>>>(ta, tb, p);
   CHASE_CHECK_LAUNCH();
 }
+
+int dgemm_tiles(int M, int N) { return ceil_div(M, DCfg::BM) * ceil_div(N, DCfg::BN); }
 
 void dgemm(const ZgemmDesc& d0, cudaStream_t st) {
   if (d0.M <= 0 || d0.N <= 0) return;

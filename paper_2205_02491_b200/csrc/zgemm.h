@@ -39,6 +39,7 @@ struct ZgemmDesc {
 void zgemm(const ZgemmDesc& d, cudaStream_t st);
 // number of CTA tiles (= fused-reduction tiles) of the 3M kernel for an M x N output
 int zgemm3m_tiles(int M, int N);
+int dgemm_tiles(int M, int N);
 // The same contract for real double (op(A) = A^T when conjA; use3m ignored).  Real-symmetric f2.
 void dgemm(const ZgemmDesc& d, cudaStream_t st);
 

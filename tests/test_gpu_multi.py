@@ -31,7 +31,7 @@ def test_two_gpu_grid(dtype):
     assert r.returncode == 0 and lines, r.stdout[-2000:] + r.stderr[-2000:]
     res = json.loads(lines[-1])
     assert res["ok"], res
-    if dtype == "c128":       # the filter ran through the fused peer all-reduce (f1)
+    if dtype in ("c128", "r64"):   # the filter ran through the fused peer all-reduce (f1)
         assert "fused peer all-reduce ready" in r.stderr
     if dtype == "c64-fused":
         assert "fused peer all-reduce ready for complex single" in r.stderr
