@@ -164,7 +164,7 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
     P.ldy = v.ld;
   }
   if (gamma == 0.0 || P.shift_lo >= P.shift_hi) P.shift_lo = P.shift_hi = 0;
-  static bool attr[2] = {false, false};
+  static unsigned long long attr[2] = {0, 0};
   // CTA pairs (default; CHASE_C64_PAIR=0 selects the single-CTA kernel)
   static const bool pair = !getenv("CHASE_C64_PAIR") || atoi(getenv("CHASE_C64_PAIR")) != 0;
   if (red && !pair) throw UsageError("fused c64 all-reduce needs the CTA-pair kernel");
@@ -172,13 +172,11 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   if (pair) {
     // CTA pairs: one cluster of 2 per 256-row x BN tile
     constexpr size_t SMEM2 = Cfg2<BN>::SMEM;
-    static bool attr2[4] = {false, false, false, false};
+    static unsigned long long attr2[4] = {0, 0, 0, 0};
     const int grid2 = 2 * ceil_div(P.M, 2 * BMR) * ceil_div(P.N, BN);
     auto go = [&](auto kern, int slot) {
-      if (!attr2[slot]) {
+      if (first_on_device(attr2[slot]))
         CHASE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
-        attr2[slot] = true;
-      }
       kern<<<grid2, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
     };
     if (dir == 0) {
@@ -191,10 +189,10 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   }
   const int grid = ceil_div(P.M, BMR) * ceil_div(P.N, BN);
   if (dir == 0) {
-    if (!attr[0]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)); attr[0] = true; }
+    if (first_on_device(attr[0])) CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<true, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     c64_step_kernel<true, BN><<<grid, C64_THREADS, SMEM, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
   } else {
-    if (!attr[1]) { CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM)); attr[1] = true; }
+    if (first_on_device(attr[1])) CHASE_CUDA(cudaFuncSetAttribute(c64_step_kernel<false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
     c64_step_kernel<false, BN><<<grid, C64_THREADS, SMEM, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
   }
   CHASE_CHECK_LAUNCH();

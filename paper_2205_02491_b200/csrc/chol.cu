@@ -134,12 +134,11 @@ __global__ void k_trinv_diag(const double2* R, int64_t ldr, double2* X, int64_t 
 bool cholesky_upper(void* Gv, int64_t ld, int n, int* d_info, cudaStream_t st) {
   double2* G = reinterpret_cast<double2*>(Gv);
   CHASE_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
-  static bool attr = false;
+  static unsigned long long attr = 0;
   const size_t smem = sizeof(double2) * NB * LDS;
-  if (!attr) {
+  if (first_on_device(attr)) {
     CHASE_CUDA(cudaFuncSetAttribute(k_chol_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CHASE_CUDA(cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
   }
   for (int kb = 0; kb < n; kb += NB) {
     const int nb = std::min(NB, n - kb);
@@ -173,10 +172,9 @@ void trinv_upper(const void* Rv, int64_t ldr, void* Xv, int64_t ldx, void* T, in
   zzero2d(X, ldx, n, n, st);
   const int nblk = ceil_div(n, NB);
   const size_t smem = 2 * sizeof(double2) * NB * LDS;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
     CHASE_CUDA(cudaFuncSetAttribute(k_trinv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
   }
   k_trinv_diag<<<nblk, NB, smem, st>>>(R, ldr, X, ldx, n);
   CHASE_CHECK_LAUNCH();

@@ -41,3 +41,14 @@ using z_t = double2;
 __host__ __device__ inline double2 zmk(double r, double i) { return make_double2(r, i); }
 
 }  // namespace chase
+
+// Per-device latch for one-time kernel attribute setup (cudaFuncSetAttribute is per device, and one
+// process may drive several GPUs): true the first time it is called on the current device.
+inline bool first_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}

@@ -381,7 +381,7 @@ struct Work {
     A = Zp = U = nullptr; pairs = order = nullptr; part = nullptr; np = b = 0;
   }
 };
-Work g_work;   // one solve at a time per process (the library is single-threaded per handle)
+Work g_works[64];   // per device; one solve at a time per device (the library is single-threaded per handle)
 }  // namespace
 
 int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz, cudaStream_t st) {
@@ -389,14 +389,16 @@ int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz,
   const int np = ceil_div(n, S) * S;
   const int b = np / S;           // pairs per round; 2b blocks of W
   const int nblocks = 2 * b;
+  int dev = 0;
+  CHASE_CUDA(cudaGetDevice(&dev));
+  Work& g_work = g_works[dev & 63];
   g_work.ensure(np, st);
-  static bool attr = false;
+  static unsigned long long attr = 0;
   const int smem = (int)(2 * sizeof(double2) * S * LD);
   const int smem_apply = 2 * S * S * 16 + 1024;
-  if (!attr) {
+  if (first_on_device(attr)) {
     CHASE_CUDA(cudaFuncSetAttribute(k_sub_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CHASE_CUDA(cudaFuncSetAttribute(k_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_apply));
-    attr = true;
   }
   // schedule: circle method over 2b blocks, 2b-1 rounds of b pairs
   const int rounds = nblocks - 1;

@@ -59,11 +59,10 @@ static void launch(const ZgemmDesc& d, cudaStream_t st) {
     make_zmatrix_tmap(&ta, d.A, d.K, d.M, d.lda, BM);          // A: K x M (op = A^H)
   }
   make_zmatrix_tmap(&tb, d.B, d.K, d.N, d.ldb, BN);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(attr_set)) {
     CHASE_CUDA(cudaFuncSetAttribute(zgemm_dmma_kernel<BM, BN, CONJ>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM));
-    attr_set = true;
   }
   ZgemmParams p;
   p.M = d.M; p.N = d.N; p.K = d.K;
@@ -90,11 +89,10 @@ static void launch3m(const ZgemmDesc& d, cudaStream_t st) {
     make_zmatrix_tmap(&ta, d.A, d.K, d.M, d.lda, CFG::BM);
   }
   make_zmatrix_tmap(&tb, d.B, d.K, d.N, d.ldb, CFG::BN);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(attr_set)) {
     CHASE_CUDA(cudaFuncSetAttribute(zgemm3m_dmma_kernel<CFG, CONJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)CFG::SMEM));
-    attr_set = true;
   }
   ZgemmParams p;
   p.M = d.M; p.N = d.N; p.K = d.K;
@@ -275,11 +273,10 @@ static bool make_dmatrix_tmap_chunked(CUtensorMap* map, const void* base, int64_
 
 template <bool TRANS, bool TMA>
 static void launch_d(const ZgemmDesc& d, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(attr_set)) {
     CHASE_CUDA(cudaFuncSetAttribute(dgemm_dmma_kernel<TRANS, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)DCfg::SMEM));
-    attr_set = true;
   }
   CUtensorMap ta{}, tb{};
   bool chunked = false;
