@@ -27,6 +27,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+CUtensorMapL2promotion promo() {
+  static const int v = getenv("CHASE_C64_PROMO") ? atoi(getenv("CHASE_C64_PROMO")) : 3;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+       : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // fp32 matrix, dim 0 = rows (contiguous), dim 1 = cols (stride ld floats); box {32, box_cols}
 void f32_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
               CUtensorMapSwizzle sw) {
@@ -35,7 +41,7 @@ void f32_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int6
   cuuint32_t box[2] = {32u, (cuuint32_t)box_cols};
   cuuint32_t es[2] = {1u, 1u};
   CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, promo(),
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (fp32) failed: " + std::to_string((int)r));
 }
@@ -131,6 +137,8 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
   P.beta_on = beta_on ? 1 : 0;
   static const int kcs = getenv("CHASE_C64_KC") ? atoi(getenv("CHASE_C64_KC")) : 0;
   P.kc_stages = kcs;
+  static const int rg = getenv("CHASE_C64_RASTER") ? atoi(getenv("CHASE_C64_RASTER")) : 0;
+  P.raster_group = rg;
   if (dir == 0) {       // forward: W = alpha (H V - gamma E V) + beta W
     f32_tmap(&ta, H, 2 * p, q, 2 * ldh, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     f32_tmap(&tal, Hlo, 2 * p, q, 2 * p, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);

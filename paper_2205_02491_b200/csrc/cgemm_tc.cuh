@@ -59,6 +59,7 @@ struct C64Params {
   int64_t ldy;              // in floats (fwd: 2*p rows; bwd: q)
   int beta_on;
   int kc_stages;            // K chunk (in BK stages) per fresh TMEM accumulator; 0 = default
+  int raster_group;         // pair kernel tile order: 0 = N fastest; g > 0 = groups of g M pairs, M fastest
   C64Red red;               // f1 (pair kernel): fused all-reduce over peer memory when red.n > 1
 };
 
@@ -510,8 +511,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
   const uint32_t rank = tc2::cluster_rank();
   const int tiles_n = (p.N + BN - 1) / BN;
   const int pair = blockIdx.x >> 1;
-  const int m0 = (pair / tiles_n) * (2 * BMR) + (int)rank * BMR;
-  const int n0 = (pair % tiles_n) * BN;
+  int pm, pn;
+  if (p.raster_group > 0) {
+    // groups of `raster_group` M pairs; inside a group M fastest, then N
+    const int tiles_mp = (p.M + 2 * BMR - 1) / (2 * BMR);
+    const int per_group = p.raster_group * tiles_n;
+    const int grp = pair / per_group, first = grp * p.raster_group;
+    const int gsize = min(tiles_mp - first, p.raster_group);
+    const int in = pair % per_group;
+    pm = first + in % gsize;
+    pn = in / gsize;
+  } else {
+    pm = pair / tiles_n;
+    pn = pair % tiles_n;
+  }
+  const int m0 = pm * (2 * BMR) + (int)rank * BMR;
+  const int n0 = pn * BN;
   const int KT = (p.K + BK - 1) / BK;
   const int NCH = (KT + CH - 1) / CH;
 
