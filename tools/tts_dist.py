@@ -53,7 +53,7 @@ def main():
         err = np.abs(vals - lam[:nev])
         print(json.dumps({"N": N, "nev": nev, "nex": nex, "family": fam, "dtype": dtype, "tol": tol,
                           "grid": f"{grid[0]}x{grid[1]}", "gpus": world, "status": st, "t_all_s": t_all,
-                          "iterations": rep["iterations"], "matvecs": rep["matvecs"],
+                          "iterations": rep["iterations"], "locked": rep["locked"], "matvecs": rep["matvecs"],
                           "phases_rank0": {k: rep[k] for k in ("t_lanczos", "t_filter", "t_qr", "t_rr", "t_resid")},
                           "filter_tflops_per_gpu": 8.0 * N * N * rep["matvecs"] / world / max(rep["t_filter"], 1e-12) / 1e12,
                           "eig_err_rel_normH": float(np.max(err) / normH),
