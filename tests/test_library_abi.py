@@ -46,3 +46,24 @@ def test_library_is_sm100a_only():
     out = subprocess.run([exe, "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     assert "sm_90" not in out and "sm_80" not in out
+
+
+def _build_example(out):
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    lib = os.path.join(root, "paper_2205_02491_b200")
+    cmd = ["gcc", "-O2", "-std=c11", os.path.join(root, "examples", "chase_example.c"),
+           "-I" + os.path.join(root, "include"), "-I/usr/local/cuda/include", "-L" + lib, "-lchase_b200",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-lm", "-Wl,-rpath," + lib, "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def test_plain_c_example_compiles_and_links(tmp_path):
+    """The boundary is a C ABI: a plain C11 program (no torch, no Python) builds against
+    include/chase.h and links libchase_b200.so."""
+    _build_example(str(tmp_path / "chase_example"))
