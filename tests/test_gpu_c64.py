@@ -162,3 +162,17 @@ def test_f4_mixed_filter_c128_solve(lib, fam, N):
     assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
     assert np.max(np.linalg.norm(H @ vecs - vecs * vals[None, :], axis=0)) <= 1e-10 * normH
     np.testing.assert_allclose(vecs.conj().T @ vecs, np.eye(nev), atol=1e-12)
+
+
+def test_c64_solve_largest(lib):
+    """`largest` (ledger #17) in complex single: the nev largest eigenvalues (ascending, as the
+    complex-double path returns them)."""
+    N, nev, nex = 800, 24, 12
+    M = make_matrix("uniform", N, "g2", seed=11)
+    H = M.dense().astype(np.complex64)
+    ch = lib.Chase(N, nev, nex, dtype="c64")
+    ch.set_option("largest", 1)
+    vals, dvecs, rep, st = ch.solve(_dev(H), nev, nex, deg=20, tol=1e-5)
+    assert st == 0, ch.last_error()
+    top = np.sort(M.lam)[-nev:]
+    assert np.max(np.abs(vals - top)) <= 2e-5 * np.max(np.abs(M.lam))
