@@ -142,7 +142,19 @@ def oracle_sample(N, seconds=12.0, rows=1024, ncols=64, family="uniform"):
             break
     flops = 8.0 * rows * N * ncols * n
     cores = len(os.sched_getaffinity(0))
-    return flops / el / 1e12, cores, f"{n} oracle filter steps (hemm_step, P:385-390) on a {rows} x {N} row panel of H times {ncols} columns, numpy complex128"
+    return flops / el / 1e12, cores, (f"{n} oracle filter steps (hemm_step, P:385-390) on a {rows} x {N} row panel of H "
+                                      f"times {ncols} columns, numpy complex128; host CPU: {_cpu_model()}")
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args, out):
