@@ -28,6 +28,8 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     grid = grid_shape(world)
+    if os.environ.get("MG_GRID"):                       # e.g. "1x4": a row communicator of 4 ranks
+        grid = tuple(int(x) for x in os.environ["MG_GRID"].split("x"))
     dtype = os.environ.get("MG_DTYPE", "c128")
     real, single = dtype == "r64", dtype == "c64"
     # c64: TMA operand layout needs q % 4 == 0 and even p -> N = 1200 by default
