@@ -268,11 +268,12 @@ __device__ __forceinline__ void c64_epilogue(const C64Params& p, int row, int nb
 // Accumulation: the tensor core's FP32 accumulator loses precision with every MMA added into it
 // (measured step error, K = 1200: 1.3e-7 / 1.9e-7 / 3.0e-7 / 5.3e-7 / 1.9e-6 for chunks of
 // 32 / 64 / 128 / 256 / 1024 real k -- linear in the chunk length; unchunked it reached 5e-6 at
-// K = 1200 and grows with K).  The K loop is therefore cut into chunks of 64: every chunk starts
+// K = 1200 and grows with K).  The K loop is therefore cut into chunks of 128 (64 costs ~4 % of
+// throughput for 1.9e-7 instead of 3.0e-7; 32 costs ~10 %): every chunk starts
 // a fresh TMEM accumulator (double-buffered, 2 x 2BN columns), and 8 epilogue warps drain the
 // finished chunk into FP32 registers with round-to-nearest adds while the next chunk accumulates.
 constexpr int C64_THREADS = 320;       // warp 0 TMA, warp 1 MMA, warps 2..9 chunk drain + epilogue
-constexpr int C64_KC_STAGES = 2;       // chunk = 2 stages x BK 32 = 64 real k (error ~ linear in chunk length)
+constexpr int C64_KC_STAGES = 4;       // chunk = 4 stages x BK 32 = 128 real k (error ~ linear in chunk length)
 
 template <bool FWD, int BN>
 __global__ void __launch_bounds__(C64_THREADS, 1)
