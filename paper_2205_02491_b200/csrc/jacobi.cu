@@ -83,15 +83,26 @@ __global__ void __launch_bounds__(SUB_T) k_sub_eig(const double2* A, int np, con
       tot += m2;
       if (i != j) off += m2;
     }
-    red[t] = off;
+    // fixed-order (deterministic) reduction: xor-shuffle within warps, then warp 0 over the 32
+    // warp sums
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    }
+    if ((t & 31) == 0) { red[t >> 5] = off; red[32 + (t >> 5)] = tot; }
     __syncthreads();
-    for (int s = SUB_T / 2; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
-    const double offs = red[0];
+    if (t < 32) {
+      double a = red[t], b = red[32 + t];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      if (t == 0) { red[64] = a; red[65] = b; }
+    }
     __syncthreads();
-    red[t] = tot;
-    __syncthreads();
-    for (int s = SUB_T / 2; s > 0; s >>= 1) { if (t < s) red[t] += red[t + s]; __syncthreads(); }
-    const double tots = red[0];
+    const double offs = red[64], tots = red[65];
     __syncthreads();
     if (offs <= 1e-32 * tots || offs == 0.0) break;
     if (sweep > 0 && nrot == 0) break;          // previous sweep found nothing above threshold
