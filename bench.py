@@ -133,6 +133,14 @@ def oracle_sample(N, seconds=12.0, rows=1024, ncols=64, family="uniform"):
     Hp = M.block(0, rows, 0, N)
     X = oracle.random_block(2, 0, N, 0, ncols, 0)
     Y = np.zeros((rows, ncols), dtype=np.complex128)
+    cores = len(os.sched_getaffinity(0))
+    # torchrun exports OMP_NUM_THREADS=1; the oracle baseline runs on all host cores regardless
+    try:
+        from threadpoolctl import threadpool_limits, threadpool_info
+        limiter = threadpool_limits(limits=cores)
+        used = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:
+        limiter, used = None, cores
     n, t0 = 0, time.perf_counter()
     while True:
         Y = oracle.hemm_step_rows(Hp, 0, X, Y, 0.5, -0.2, 0.3)
@@ -140,8 +148,10 @@ def oracle_sample(N, seconds=12.0, rows=1024, ncols=64, family="uniform"):
         el = time.perf_counter() - t0
         if el >= seconds:
             break
+    if limiter is not None:
+        limiter.restore_original_limits()
+    cores = used
     flops = 8.0 * rows * N * ncols * n
-    cores = len(os.sched_getaffinity(0))
     return flops / el / 1e12, cores, (f"{n} oracle filter steps (hemm_step, P:385-390) on a {rows} x {N} row panel of H "
                                       f"times {ncols} columns, numpy complex128; host CPU: {_cpu_model()}")
 
