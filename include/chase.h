@@ -136,7 +136,12 @@ chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H_shard, 
  * V-layout q x ncols (ldv); W: device W-layout workspace p x ncols (ldw), overwritten.
  * degrees: host, ncols even integers >= 0 sorted ascending (Alg. 1 line 14).  Column a
  * receives the damped scaled Chebyshev polynomial of degree m_a (ledger #1), ends in V-layout.
- * matvecs (may be NULL) receives sum_a m_a. */
+ * matvecs (may be NULL) receives sum_a m_a.  On a multi-GPU grid with fused_reduce=1
+ * (complex double / real) the block is staged through the library's V / W workspace, whose
+ * replicas the step kernels sum into over peer memory (f1); W is then not written.  CHASE_C64
+ * uses internal operand formats (W unused).  Errors: CHASE_E_USAGE for unsorted / odd degrees,
+ * an empty interval (b_sup <= mu_ne) or bad leading dimensions; CHASE_E_NCCL if a peer stops
+ * arriving in the fused all-reduce (20 s). */
 chase_status chase_filter(chase_handle* h, const void* H_shard, int64_t ldh, void* V, int64_t ldv,
                           void* W, int64_t ldw, int32_t ncols, const int32_t* degrees,
                           double b_sup, double mu_1, double mu_ne, int64_t* matvecs);
