@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c64", action="store_true", help="skip the complex-single filter sub-measurement")
+    ap.add_argument("--ref-seconds", type=float, default=None, help=argparse.SUPPRESS)   # tests: bound the oracle sample
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: N = n sqrt(G) (paper P:717-718, default); strong: N = n on every G (config 3)")
     return ap.parse_args()
@@ -175,6 +176,8 @@ def run_reference(args, out):
     from paper_2205_02491_b200.dist import weak_scaled_n, grid_shape
     N = weak_scaled_n(args.n, world) if args.scaling == "weak" else args.n
     per = max(3.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    if args.ref_seconds:
+        per = args.ref_seconds
     for _ in range(args.warmup):
         oracle_sample(N, seconds=per / 3, family=args.family)
     vals, cores, sample = [], 0, ""
