@@ -127,7 +127,8 @@ chase_status chase_solve(chase_handle* h, const void* H_shard, int64_t ldh, int6
  *   dir = 1 (backward, Eq. v=aw):  Y_j = alpha (H_ij^H X_i - gamma E_ij^T X_i) [+ beta Y_j on i = i*(j)],
  *           X W-layout, Y V-layout; sum over the column comm.
  * E_ij is the restriction of I_N to the shard (nonzero on the global-diagonal crossing I_ij);
- * H is never modified.  On return Y holds the full result, replicated. */
+ * H is never modified.  On return Y holds the full result, replicated.  ncols = 0 is a no-op
+ * (CHASE_OK; pointers may be NULL, nothing is read or written). */
 chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H_shard, int64_t ldh,
                              const void* X, int64_t ldx, void* Y, int64_t ldy, int32_t ncols,
                              double alpha, double beta, double gamma);
@@ -141,7 +142,8 @@ chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H_shard, 
  * replicas the step kernels sum into over peer memory (f1); W is then not written.  CHASE_C64
  * uses internal operand formats (W unused).  Errors: CHASE_E_USAGE for unsorted / odd degrees,
  * an empty interval (b_sup <= mu_ne) or bad leading dimensions; CHASE_E_NCCL if a peer stops
- * arriving in the fused all-reduce (20 s). */
+ * arriving in the fused all-reduce (20 s).  ncols = 0 is a no-op (CHASE_OK, *matvecs = 0, no
+ * argument is read). */
 chase_status chase_filter(chase_handle* h, const void* H_shard, int64_t ldh, void* V, int64_t ldv,
                           void* W, int64_t ldw, int32_t ncols, const int32_t* degrees,
                           double b_sup, double mu_1, double mu_ne, int64_t* matvecs);
@@ -152,7 +154,8 @@ chase_status chase_lanczos(chase_handle* h, const void* H_shard, int64_t ldh, in
                            double* b_sup, double* mu_1, double* mu_ne, double* nu);
 
 /* Fill a V-layout block (q x ncols, ldv) with the counter-based start block (Philox4x32-10 keyed
- * by (seed, global row, column, stream)). */
+ * by (seed, global row, column, stream)).  ncols = 0 is a
+ * no-op. */
 chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t col0, int32_t ncols,
                                 uint64_t seed, uint32_t stream);
 

@@ -452,6 +452,7 @@ chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H, int64_
   return guarded(h, [&]() {
     const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
     if (dir != 0 && dir != 1) throw UsageError("dir must be 0 or 1");
+    if (ncols == 0) return CHASE_OK;   // empty block: no-op, pointers may be NULL
     if (!H || !X || !Y || ncols < 0 || ldh < p) throw UsageError("bad pointers / sizes");
     if (ldx < (dir == 0 ? q : p) || ldy < (dir == 0 ? p : q)) throw UsageError("bad leading dimension");
     order_after_user(h);
@@ -469,7 +470,11 @@ chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, 
                           double b_sup, double mu_1, double mu_ne, int64_t* matvecs) {
   return guarded(h, [&]() {
     const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
-    if (!H || !V || !W || ncols < 0 || (ncols > 0 && !degrees)) throw UsageError("bad pointers");
+    if (ncols == 0) {                  // empty block: no-op, pointers may be NULL
+      if (matvecs) *matvecs = 0;
+      return CHASE_OK;
+    }
+    if (!H || !V || !W || ncols < 0 || !degrees) throw UsageError("bad pointers");
     if (ldh < p || ldv < q || ldw < p) throw UsageError("bad leading dimension");
     order_after_user(h);
     const Grid& g = h->grid;
@@ -513,6 +518,7 @@ chase_status chase_lanczos(chase_handle* h, const void* H, int64_t ldh, int32_t 
 chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t col0, int32_t ncols,
                                 uint64_t seed, uint32_t stream) {
   return guarded(h, [&]() {
+    if (ncols == 0) return CHASE_OK;   // empty block: no-op, V may be NULL
     if (!V || ldv < h->grid.cols.len || ncols < 0) throw UsageError("bad arguments");
     order_after_user(h);
     random_block(h, V, ldv, h->grid.cols.len, h->grid.cols.start, col0, ncols, seed, stream, h->c64());

@@ -106,6 +106,31 @@ def test_filter_rejects_odd_or_unsorted_degrees(lib):
         ch.filter(dH, dV, dW, [4, 2, 4, 4], 2.0, 0.0, 1.0)
 
 
+def test_empty_block_and_degree_zero(lib):
+    """Degenerate cases of the filter (Alg. 1 line 4): an empty block is a no-op through
+    every entry point, and degree 0 is C_0 = 1 (the column is returned bitwise unchanged, 0
+    matvecs)."""
+    N = 300
+    H = make_matrix("uniform", N, "g2", seed=11).dense()
+    ch = lib.Chase(N, 4, 4)
+    dH = _dev(H)
+    empty = torch.zeros((N, 0), dtype=torch.complex128, device="cuda")
+    for d in (0, 1):
+        ch.hemm_step(d, dH, empty, empty, 0, 1.0, 0.5, 0.25)
+    dW = torch.zeros((N, 8), dtype=torch.complex128, device="cuda").t().contiguous().t()
+    assert ch.filter(dH, empty, dW, [], 2.0, 0.0, 1.0) == 0
+    ch.random_block(empty, 0, 0, 1, 0)
+    rng = np.random.default_rng(5)
+    V = rng.standard_normal((N, 8)) + 1j * rng.standard_normal((N, 8))
+    dV = _dev(V)
+    lam = make_matrix("uniform", N, "g2", seed=11).lam
+    assert ch.filter(dH, dV, dW, [0] * 8, lam[-1] * 1.01, lam[0], lam[8]) == 0
+    assert np.array_equal(_host(dV), V)
+    with pytest.raises(lib.ChaseError):         # empty interval b_sup <= mu_ne (chase.h)
+        ch.filter(dH, dV, dW, [2] * 8, lam[8], lam[0], lam[8])
+    ch.close()
+
+
 @pytest.mark.parametrize("grid", [(1, 2), (2, 1), (2, 2), (2, 3), (3, 2)])
 def test_emulated_grid_hemm_step(lib, grid):
     """Grid neutrality of the fused step: per-rank partials (emulated-grid mode) summed
