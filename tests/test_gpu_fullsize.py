@@ -63,6 +63,35 @@ def test_fullsize_step_sampled_rows(big, direction):
     ch.close()
 
 
+@pytest.mark.parametrize("direction", [0, 1])
+def test_fullsize_c64_step_sampled_rows(big, direction):
+    """Complex-single fused step (a2 / a4 on tcgen05) at the shape bench.py's
+    c64_filter line times: sampled rows vs the oracle's complex128 step on the complex64-rounded
+    rows of H (rounded on the host from the generator).  Bar 1e-5 (the c64 step bar)."""
+    pkg, M, H = big
+    H32 = H.to(torch.complex64)
+    ch = pkg.Chase(N, NCOL - 750, 750, dtype="c64")
+    X = _rand(N, NCOL, 31).to(torch.complex64)
+    Y0 = _rand(N, NCOL, 32).to(torch.complex64)
+    Y = Y0.clone()
+    alpha, beta, gamma = 0.0123, -0.77, 0.4321
+    ch.hemm_step(direction, H32, X, Y, NCOL, alpha, beta, gamma)
+    rows = np.sort(np.random.default_rng(10 + direction).choice(N, 32, replace=False))
+    Xh = X.cpu().numpy().astype(np.complex128)
+    Yh, Y0h = Y.cpu().numpy().astype(np.complex128), Y0.cpu().numpy().astype(np.complex128)
+    err = num = 0.0
+    for r in rows:
+        Hrow = M.block(int(r), 1, 0, N) if direction == 0 else M.block(0, N, int(r), 1).conj().T
+        Hrow = Hrow.astype(np.complex64).astype(np.complex128)
+        ref = oracle.hemm_step_rows(Hrow, int(r), Xh, Y0h[r:r + 1], alpha, beta, gamma)
+        err += np.sum(np.abs(Yh[r:r + 1] - ref) ** 2)
+        num += np.sum(np.abs(ref) ** 2)
+    assert np.sqrt(err / num) <= 1e-5, np.sqrt(err / num)
+    ch.close()
+    del H32, X, Y, Y0
+    torch.cuda.empty_cache()
+
+
 def test_fullsize_filter_eigencombinations(big):
     pkg, M, H = big
     ch = pkg.Chase(N, NCOL - 750, 750)
