@@ -67,3 +67,22 @@ def test_plain_c_example_compiles_and_links(tmp_path):
     """The boundary is a C ABI: a plain C11 program (no torch, no Python) builds against
     include/chase.h and links libchase_b200.so."""
     _build_example(str(tmp_path / "chase_example"))
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No fallback path: with the shared library absent the binding raises instead of computing."""
+    from paper_2205_02491_b200 import _lib
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "libchase_b200.so"))
+    with pytest.raises(ImportError, match="no fallback"):
+        _lib.load()
+
+
+def test_product_package_never_references_the_oracle():
+    """The product path (package sources, CUDA included) shares nothing with oracle/."""
+    pkg_dir = os.path.join(ROOT, "paper_2205_02491_b200")
+    for dirpath, _, files in os.walk(pkg_dir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f), errors="replace").read()
+                assert not re.search(r"^\s*(?:import|from)\s+oracle\b|#include\s+[\"<][^\">]*oracle", src, re.M), f
