@@ -136,3 +136,34 @@ def test_fullsize_solve_config2(big):
     G = (Vs.conj().T @ Vs).cpu().numpy()
     assert np.max(np.abs(G - np.eye(len(cols)))) <= 1e-12
     ch.close()
+
+
+@pytest.mark.parametrize("direction", [0, 1])
+def test_fullsize_real_step_sampled_rows(direction):
+    """Real-symmetric fused step (CHASE_R64 DMMA kernel) at N = 30000 x 3000: sampled
+    rows vs the oracle's float64 step on the generator's rows of H (R2, host side)."""
+    import paper_2205_02491_b200 as pkg
+    from chase_gen.dense import R2Matrix
+    from chase_gen.device import DeviceR2
+    M = R2Matrix(spectrum("uniform", N), seed=2)
+    H = torch.empty((N, N), dtype=torch.float64, device="cuda").t()
+    DeviceR2(M).fill(H, 0, 0)
+    g = torch.Generator(device="cuda").manual_seed(40 + direction)
+    X = torch.randn((NCOL, N), dtype=torch.float64, device="cuda", generator=g).t()
+    Y0 = torch.randn((NCOL, N), dtype=torch.float64, device="cuda", generator=g).t()
+    Y = Y0.clone()
+    ch = pkg.Chase(N, NCOL - 750, 750, dtype="r64")
+    alpha, beta, gamma = 0.0123, -0.77, 0.4321
+    ch.hemm_step(direction, H, X, Y, NCOL, alpha, beta, gamma)
+    rows = np.sort(np.random.default_rng(20 + direction).choice(N, 48, replace=False))
+    Xh, Yh, Y0h = X.cpu().numpy(), Y.cpu().numpy(), Y0.cpu().numpy()
+    err = num = 0.0
+    for r in rows:
+        Hrow = M.block(int(r), 1, 0, N) if direction == 0 else M.block(0, N, int(r), 1).T
+        ref = oracle.hemm_step_rows(Hrow, int(r), Xh, Y0h[r:r + 1], alpha, beta, gamma)
+        err += np.sum((Yh[r:r + 1] - ref) ** 2)
+        num += np.sum(ref ** 2)
+    assert np.sqrt(err / num) <= 1e-13, np.sqrt(err / num)
+    ch.close()
+    del H, X, Y, Y0
+    torch.cuda.empty_cache()
