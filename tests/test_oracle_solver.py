@@ -52,6 +52,44 @@ def test_lanczos_full_krylov(golden):
     assert lz.mu_1 == pytest.approx(1.0, abs=1e-10)
 
 
+@pytest.mark.parametrize("n_e", [1, 3, 5, 7, 9])
+def test_lanczos_dos_quantile_uniform_weights(n_e):
+    """mu_ne pin (ledger #14): full Krylov on diag(1..10) from all-ones start vectors.
+    Every eigenvector carries the same share 1/N of the start vector, so the Ritz values are the
+    exact eigenvalues, each DoS weight is exactly 1/(N L), the CDF after the L copies of lambda_k is
+    k/N, and the n_e/N quantile is lambda_{n_e} = n_e.  b_sup = lambda_max + |beta_m| = 10."""
+    N, L = 10, 4
+    A = np.diag(np.arange(1.0, N + 1.0)).astype(complex)
+    lz = oracle.lanczos(A, n_e, steps=N, runs=L, start=np.ones((N, L), dtype=complex))
+    assert lz.mu_ne == pytest.approx(float(n_e), abs=1e-10)
+    assert lz.mu_1 == pytest.approx(1.0, abs=1e-10)
+    assert lz.b_sup == pytest.approx(10.0, abs=1e-8)
+    np.testing.assert_allclose(lz.weights, 1.0 / (N * L), atol=1e-13)
+
+
+@pytest.mark.parametrize("rotated", [False, True])
+@pytest.mark.parametrize("n_e,expect", [(1, 3), (2, 5), (3, 6), (5, 7), (8, 9)])
+def test_lanczos_dos_quantile_weighted_start(rotated, n_e, expect):
+    """mu_ne pin with unequal weights: start vector s = Q (sqrt(k))_k on H = Q diag(1..10) Q^H.
+    Full Krylov makes the Ritz values exact and the weight of lambda_k equal to k / sum(k) = k/55,
+    so CDF(k) = k(k+1)/110 and mu_ne = smallest k with k(k+1)/110 >= n_e/10, worked by hand:
+    n_e = 1 -> 3 (12/110 >= 0.1 > 6/110), 2 -> 5 (30/110 >= 0.2 > 20/110), 3 -> 6 (42/110 >= 0.3),
+    5 -> 7 (56/110 >= 0.5 > 42/110), 8 -> 9 (90/110 >= 0.8 > 72/110).
+    The rotated case (Haar Q) catches a conjugation / transposition slip in the weights."""
+    N, L = 10, 2
+    lam = np.arange(1.0, N + 1.0)
+    Q = np.eye(N, dtype=complex)
+    if rotated:
+        rng = np.random.default_rng(7)
+        Q, R = np.linalg.qr(rng.standard_normal((N, N)) + 1j * rng.standard_normal((N, N)))
+    A = (Q * lam[None, :]) @ Q.conj().T
+    s = Q @ np.sqrt(lam).astype(complex)
+    lz = oracle.lanczos(A, n_e, steps=N, runs=L, start=np.stack([s, 2.5 * s], axis=1))
+    assert lz.mu_ne == pytest.approx(float(expect), abs=1e-9)
+    for k in range(1, N + 1):      # each eigenvalue's pooled weight: L copies of k/55 / L
+        assert np.sum(lz.weights[np.abs(lz.ritz - k) < 1e-6]) == pytest.approx(k / 55.0, abs=1e-12)
+
+
 @pytest.mark.parametrize("fam", ["uniform", "geometric", "121", "wilkinson"])
 def test_lanczos_bounds_bracket_spectrum(fam):
     """b_sup >= lambda_max (else the filter amplifies the unwanted end) and mu_1 >= lambda_1."""
