@@ -68,7 +68,8 @@ typedef struct {
   chase_dtype dtype;              /* CHASE_C128, CHASE_C64 or CHASE_R64 */
   int64_t N;                      /* matrix order */
   int32_t nev_max, nex_max;       /* workspace sizing */
-  int32_t grid_rows, grid_cols;   /* r, c; 0,0 = 1 x world.  world_size == 1 with r*c > 1 selects
+  int32_t grid_rows, grid_cols;   /* r, c; 0,0 = auto: r * c = world, r <= c, |r - c| minimal
+                                     (ledger #19).  world_size == 1 with r*c > 1 selects
                                      the emulated-grid mode: the handle owns shard `rank` of an
                                      r x c grid and all cross-rank sums are skipped (each call
                                      returns this rank's partial) -- for single-GPU testing. */
@@ -78,6 +79,15 @@ typedef struct {
   void* cuda_stream;              /* cudaStream_t the caller produces inputs on (e.g. torch's current
                                      stream); every call waits for work already queued on it.
                                      NULL = the legacy default stream. */
+  int32_t colocated;              /* 0: one process per rank, NCCL communicators (production).
+                                     1: the world_size ranks are threads of THIS process, each with
+                                     its own handle (usually all on one device, which NCCL refuses):
+                                     the communicators are an in-process group keyed by the 128
+                                     bytes at nccl_unique_id (any bytes shared by the ranks), sums
+                                     taken in rank order (replicas bitwise identical), and the fused
+                                     f1 reduction uses the co-located handles' own device pointers.
+                                     Every collective call must then be made concurrently by all
+                                     ranks' threads.  For single-GPU testing of the grid data plane. */
 } chase_init_args;
 
 typedef struct {
@@ -104,7 +114,14 @@ chase_status chase_init(chase_handle** out, const chase_init_args* args);
  * fused_reduce=1 (on a grid the complex-double filter steps sum their partial products
  * inside the GEMM epilogue over peer memory -- CUDA IPC over NVLink -- instead of ncclAllReduce),
  * fused_reduce_c64=0 (the same for the complex-single filter; off by default: measured slower
- * than ncclAllReduce + local format rebuild at N = 170000 on 2x2). */
+ * than ncclAllReduce + local format rebuild at N = 170000 on 2x2),
+ * peer_timeout=120 (seconds a rank's fused-reduce wait tolerates a peer that stopped arriving;
+ * then CHASE_E_NCCL on every rank and no further fused steps are issued; each fused filter call
+ * also starts with a world barrier so host-side skew between calls does not count),
+ * comm_timeout=0 (host waits poll ncclCommGetAsyncError; a value > 0 also fails a wait that
+ * exceeds it, e.g. when a peer died -- its communicators are aborted on CUDA/NCCL errors).
+ * Complex-double grids fall back from the fused reduction to ncclAllReduce when a step would have
+ * more tiles than the 2^17 arrival counters per communicator. */
 chase_status chase_set_option(chase_handle* h, const char* key, double value);
 
 /* This rank's shard: rows [row0, row0+p) and columns [col0, col0+q) of H. */

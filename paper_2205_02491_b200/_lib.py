@@ -32,7 +32,7 @@ class InitArgs(C.Structure):
     _fields_ = [("dtype", C.c_int), ("N", C.c_int64), ("nev_max", C.c_int32), ("nex_max", C.c_int32),
                 ("grid_rows", C.c_int32), ("grid_cols", C.c_int32), ("rank", C.c_int32),
                 ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p), ("cuda_device", C.c_int32),
-                ("cuda_stream", C.c_void_p)]
+                ("cuda_stream", C.c_void_p), ("colocated", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -104,7 +104,7 @@ class Chase:
     C128, C64, R64 = 0, 1, 2  # chase_dtype: complex double / complex single (tcgen05) / real symmetric
 
     def __init__(self, N, nev_max, nex_max, grid=(1, 1), rank=0, world_size=1, nccl_id=None,
-                 device=0, stream=None, dtype="c128"):
+                 device=0, stream=None, dtype="c128", colocated=False):
         self.lib = load()
         self._h = C.c_void_p()
         self._id = None
@@ -120,6 +120,7 @@ class Chase:
             self._id = C.create_string_buffer(bytes(nccl_id), 128)
             args.nccl_unique_id = C.cast(self._id, C.c_void_p)
         args.cuda_device = int(device)
+        args.colocated = 1 if colocated else 0
         if stream is None:
             # order every library call after the caller's current torch stream (inputs written by
             # torch kernels must be complete before the library's own stream reads them)

@@ -231,18 +231,9 @@ static bool c64_pair_kernel() {
 }  // namespace
 
 // in-place float sum of a complex64 column block (rows x ncols, ld) over a communicator
-void allreduce_c64(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows, int64_t ld, int ncols) {
-  if (comm_size <= 1 || !comm || ncols <= 0 || rows <= 0) return;
-  if (ld == rows) {
-    CHASE_NCCL(ncclAllReduce(Y, Y, (size_t)(2 * rows * ncols), ncclFloat, ncclSum, comm, h->stream));
-    return;
-  }
-  CHASE_NCCL(ncclGroupStart());
-  for (int c = 0; c < ncols; ++c) {
-    float* col = reinterpret_cast<float*>(Y) + 2 * (int64_t)c * ld;
-    CHASE_NCCL(ncclAllReduce(col, col, (size_t)(2 * rows), ncclFloat, ncclSum, comm, h->stream));
-  }
-  CHASE_NCCL(ncclGroupEnd());
+void allreduce_c64(chase_handle* h, const Comm& comm, void* Y, int64_t rows, int64_t ld, int ncols) {
+  if (!comm.active() || ncols <= 0 || rows <= 0) return;
+  comm_allreduce(comm, Y, 2 * rows, 2 * ld, ncols, DT::F32, Op::Sum, h->stream);
 }
 
 // f4: complex64 shadow of a complex128 shard (rounded to nearest), ld p
@@ -261,6 +252,12 @@ const void* c64_shadow(chase_handle* h, const void* H, int64_t ldh) {
 }
 
 // H_lo for the shard (recomputed when the caller's H pointer or ld changes)
+void c64_check_call(chase_handle* h, const void* H, int64_t ldh, int ncols) {
+  if (ldh % 2 != 0 || (reinterpret_cast<uintptr_t>(H) % 16) != 0)
+    throw UsageError("CHASE_C64 needs an even ldh and a 16-byte aligned H shard");
+  if (ncols > h->n_e_max) throw UsageError("c64: ncols exceeds nev_max + nex_max");
+}
+
 const void* c64_hlo(chase_handle* h, const void* H, int64_t ldh) {
   const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
   // TMA: 16-byte aligned bases / strides for the fp32 planes (ld q), the interleaved W (ld 2p
@@ -324,7 +321,7 @@ void c64_hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const v
     CHASE_CHECK_LAUNCH();
     WFmt out{reinterpret_cast<float2*>(Y), nullptr, nullptr, nullptr, ldy};
     c64_step_local(h, 0, H, ldh, Hlo, v, out, ncols, alpha * hs, beta, gamma * hs, beta_owner && beta != 0.0);
-    allreduce_c64(h, h->rowc, g.c, Y, p, ldy, ncols);
+    allreduce_c64(h, h->rowc, Y, p, ldy, ncols);
   } else {
     k_to_wfmt<<<grid_for(p * ncols), 256, 0, h->stream>>>(reinterpret_cast<const float2*>(X), ldx, p, ncols, w.w, w.wr,
                                                           w.wl, w.wrl, w.ld);
@@ -339,7 +336,7 @@ void c64_hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const v
     k_from_planar<<<grid_for(q * ncols), 256, 0, h->stream>>>(reinterpret_cast<float2*>(Y), ldy, q, ncols, v.r, v.i,
                                                               v.ld);
     CHASE_CHECK_LAUNCH();
-    allreduce_c64(h, h->colc, g.r, Y, q, ldy, ncols);
+    allreduce_c64(h, h->colc, Y, q, ldy, ncols);
   }
 }
 
@@ -358,7 +355,7 @@ void c64_forward_mixed(chase_handle* h, const void* H, int64_t ldh, const double
   CHASE_CHECK_LAUNCH();
   WFmt out{w.w, nullptr, nullptr, nullptr, w.ld};
   c64_step_local(h, 0, H, ldh, Hlo, v, out, ncols, hs, 0.0, 0.0, false);
-  allreduce_c64(h, h->rowc, g.c, w.w, p, w.ld, ncols);
+  allreduce_c64(h, h->rowc, w.w, p, w.ld, ncols);
   k_convert<<<grid_for(p * ncols), 256, 0, h->stream>>>(Y, ldy, w.w, w.ld, p, ncols);
   CHASE_CHECK_LAUNCH();
 }
@@ -407,7 +404,11 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
   int first = 0;
   // f1: all-reduce inside the step kernel over peer memory (CTA-pair kernel only)
   wfmt(h, ncap, 0);
-  const bool fused = (g.r > 1 || g.c > 1) && h->opt.fused_reduce_c64 && c64_pair_kernel() && peer_c64_ready(h);
+  const int64_t pmax = (g.N + g.r - 1) / g.r, qmax = (g.N + g.c - 1) / g.c;   // same on every rank
+  const bool fused = (g.r > 1 || g.c > 1) && h->opt.fused_reduce_c64 && c64_pair_kernel() &&
+                     peer_tiles_fit(std::max(c64_step_tiles((int)(2 * pmax), ncols), c64_step_tiles((int)qmax, ncols))) &&
+                     peer_c64_ready(h);
+  if (fused) peer_enter(h);
   const int64_t plane = 2 * std::max(p, q) * (int64_t)ncap;
   for (int k = 1; k <= kmax; ++k) {
     while (first < ncols && degrees[first] < k) ++first;
@@ -426,6 +427,7 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
     WFmt w = wfmt(h, ncap, first);
     const int cn = (k & 1) ? g.c : g.r;
     if (fused && cn > 1) {
+      peer_poll(h);
       const PeerRed& pr = (k & 1) ? h->peer.row : h->peer.col;
       C64Red R;
       R.n = pr.n;
@@ -467,20 +469,18 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
     }
     if (k & 1) {
       c64_step_local(h, 0, H, ldh, Hlo, v, w, nk, alpha * hs, beta, c * hs, g.beta_owner_fwd() && beta != 0.0);
-      if (g.c > 1 && h->rowc) {
+      if (g.c > 1 && h->rowc.active()) {
         // the sum must also reach the rotated / lo copies: all-reduce W, then rebuild them
-        allreduce_c64(h, h->rowc, g.c, w.w, p, w.ld, nk);
+        allreduce_c64(h, h->rowc, w.w, p, w.ld, nk);
         k_to_wfmt<<<grid_for(p * nk), 256, 0, h->stream>>>(w.w, w.ld, p, nk, nullptr, w.wr, w.wl, w.wrl, w.ld);
         CHASE_CHECK_LAUNCH();
       }
     } else {
       c64_step_local(h, 1, H, ldh, Hlo, v, w, nk, alpha * hs, beta, c * hs, g.beta_owner_bwd() && beta != 0.0);
-      if (g.r > 1 && h->colc) {
+      if (g.r > 1 && h->colc.active()) {
         // planar Re / Im planes (ld q): sum both, then rebuild the lo planes
-        CHASE_NCCL(ncclGroupStart());
-        CHASE_NCCL(ncclAllReduce(v.r, v.r, (size_t)q * nk, ncclFloat, ncclSum, h->colc, h->stream));
-        CHASE_NCCL(ncclAllReduce(v.i, v.i, (size_t)q * nk, ncclFloat, ncclSum, h->colc, h->stream));
-        CHASE_NCCL(ncclGroupEnd());
+        comm_allreduce(h->colc, v.r, q, v.ld, nk, DT::F32, Op::Sum, h->stream);
+        comm_allreduce(h->colc, v.i, q, v.ld, nk, DT::F32, Op::Sum, h->stream);
         k_lo<<<grid_for(q * nk), 256, 0, h->stream>>>(v.rl, v.r, q, nk, v.ld, v.ld);
         CHASE_CHECK_LAUNCH();
         k_lo<<<grid_for(q * nk), 256, 0, h->stream>>>(v.il, v.i, q, nk, v.ld, v.ld);

@@ -16,25 +16,15 @@ namespace chase {
 unsigned long long g_kernel_launches = 0;
 
 // ------------------------------------------------------------------------------ collectives
-void allreduce_block(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows,
-                     int64_t ld, int ncols) {
-  if (comm_size <= 1 || !comm || ncols <= 0 || rows <= 0) return;   // !comm: emulated grid
+void allreduce_block(chase_handle* h, const Comm& comm, void* Y, int64_t rows, int64_t ld, int ncols) {
+  if (!comm.active() || ncols <= 0 || rows <= 0) return;   // inactive: emulated grid
   const int nd = h->nd();
-  if (ld == rows) {
-    CHASE_NCCL(ncclAllReduce(Y, Y, (size_t)(nd * rows * ncols), ncclDouble, ncclSum, comm, h->stream));
-    return;
-  }
-  CHASE_NCCL(ncclGroupStart());
-  for (int c = 0; c < ncols; ++c) {
-    double* col = reinterpret_cast<double*>(Y) + (int64_t)c * ld * nd;
-    CHASE_NCCL(ncclAllReduce(col, col, (size_t)(nd * rows), ncclDouble, ncclSum, comm, h->stream));
-  }
-  CHASE_NCCL(ncclGroupEnd());
+  comm_allreduce(comm, Y, nd * rows, nd * ld, ncols, DT::F64, Op::Sum, h->stream);
 }
 
-void allreduce_doubles(chase_handle* h, ncclComm_t comm, int comm_size, double* x, size_t n) {
-  if (comm_size <= 1 || !comm || n == 0) return;
-  CHASE_NCCL(ncclAllReduce(x, x, n, ncclDouble, ncclSum, comm, h->stream));
+void allreduce_doubles(chase_handle* h, const Comm& comm, double* x, size_t n) {
+  if (!comm.active() || n == 0) return;
+  comm_allreduce(comm, x, (int64_t)n, (int64_t)n, 1, DT::F64, Op::Sum, h->stream);
 }
 
 // complex (3M / 4M) or real GEMM by the handle's dtype
@@ -83,9 +73,9 @@ void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void*
   const Grid& g = h->grid;
   gemm(h, step_desc(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma));
   if (dir == 0)
-    allreduce_block(h, h->rowc, g.c, Y, g.rows.len, ldy, ncols);     // row communicator
+    allreduce_block(h, h->rowc, Y, g.rows.len, ldy, ncols);     // row communicator
   else
-    allreduce_block(h, h->colc, g.r, Y, g.cols.len, ldy, ncols);     // column communicator
+    allreduce_block(h, h->colc, Y, g.cols.len, ldy, ncols);     // column communicator
 }
 
 // ------------------------------------------------------------------------ Chebyshev filter
@@ -117,7 +107,7 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
   // boundaries; each chunk's all-reduce runs on the comm stream while the next chunk's GEMM runs,
   // and step k's GEMM on chunk c waits only for step k-1's all-reduce of chunk c (columns are
   // independent through the whole recurrence).
-  const bool comm = h->comm_stream && (g.r > 1 || g.c > 1) && h->world;
+  const bool comm = h->comm_stream && (g.r > 1 || g.c > 1) && h->world.active();
   // Chunking costs GEMM tile/wave efficiency (~1-2 % per extra chunk), so it is only worth it when
   // the all-reduce is a visible fraction of a step: t_comm / t_gemm ~ (16 B/elem / ~600 GB/s) /
   // (8 K flop/elem / ~40 TF/s) ~ 133 / K.  Measured on B200 (2x2 grid, K = 30000) it is 0.4 %, so
@@ -136,9 +126,18 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
     const char* s = reinterpret_cast<const char*>(b.p);
     return b.p && c >= s && c < s + b.bytes;
   };
+  // The arrival counters hold kCtrPerComm tiles per communicator: a step with more tiles (the
+  // largest is step 1, all columns, on the largest shard of the grid -- the same answer on every
+  // rank) all-reduces with NCCL instead.
+  const int64_t pmax = (g.N + g.r - 1) / g.r, qmax = (g.N + g.c - 1) / g.c;
+  const int max_tiles = h->real() ? std::max(dgemm_tiles((int)pmax, ncols), dgemm_tiles((int)qmax, ncols))
+                                  : std::max(zgemm3m_tiles((int)pmax, ncols), zgemm3m_tiles((int)qmax, ncols));
   const bool fused = comm && ldv == g.cols.len && ldw == g.rows.len && inside(h->V, V) && inside(h->W, W) &&
-                     peer_reduce_ready(h);
-  if (fused) nchunks = 1;
+                     peer_tiles_fit(max_tiles) && peer_reduce_ready(h);
+  if (fused) {
+    nchunks = 1;
+    peer_enter(h);                // every rank has entered this filter call (peer-timeout skew guard)
+  }
   std::vector<int> bnd(nchunks + 1);
   for (int c = 0; c <= nchunks; ++c) bnd[c] = (int)((int64_t)ncols * c / nchunks);
   bool rec[2][chase_handle::MAX_CHUNKS] = {};
@@ -169,6 +168,7 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       ZgemmDesc d = step_desc(h, dir, H, ldh, X + (int64_t)first * ldx * es, ldx, Yk, ldy, ncols - first, alpha,
                               beta, c);
       d.red = peer_red_for(h, dir, Yk);
+      peer_poll(h);                               // a timed-out wait stops the launches here
       if (d.red) {
         gemm(h, d);
         peer_wait(h, h->real() ? dgemm_tiles(d.M, d.N) : zgemm3m_tiles(d.M, d.N));
@@ -189,9 +189,9 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       cudaStream_t saved = h->stream;
       h->stream = h->comm_stream;               // allreduce_block enqueues on h->stream
       if (dir == 0)
-        allreduce_block(h, h->rowc, g.c, Y + (int64_t)lo * ldy * es, rows, ldy, hi - lo);
+        allreduce_block(h, h->rowc, Y + (int64_t)lo * ldy * es, rows, ldy, hi - lo);
       else
-        allreduce_block(h, h->colc, g.r, Y + (int64_t)lo * ldy * es, rows, ldy, hi - lo);
+        allreduce_block(h, h->colc, Y + (int64_t)lo * ldy * es, rows, ldy, hi - lo);
       h->stream = saved;
       CHASE_CUDA(cudaEventRecord(h->ev_comm[k & 1][ch], h->comm_stream));
       rec[k & 1][ch] = true;
@@ -262,18 +262,21 @@ void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t g
 // ============================================================================== C ABI
 namespace {
 
-// Collective status agreement: every rank returns the same status (chase.h "Validation").
+// Collective status agreement: every rank returns the same status (chase.h "Validation").  A
+// broken handle cannot communicate (its communicators were aborted, see fail_hard).
 chase_status agree(chase_handle* h, chase_status st) {
-  if (!h || h->world_size <= 1 || !h->world || h->broken) return st;
+  if (!h || h->world_size <= 1 || !h->world.active() || h->broken) return st;
   try {
-    int* d = nullptr;
-    CHASE_CUDA(cudaMallocAsync(&d, sizeof(int), h->stream));
+    h->peer.flag.alloc(sizeof(int));
     int v = (int)st;
-    CHASE_CUDA(cudaMemcpyAsync(d, &v, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-    CHASE_NCCL(ncclAllReduce(d, d, 1, ncclInt32, ncclMax, h->world, h->stream));
-    CHASE_CUDA(cudaMemcpyAsync(&v, d, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CHASE_CUDA(cudaFreeAsync(d, h->stream));
-    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->world.local) {
+      v = comm_allreduce_int(h->world, v, Op::Max, h->peer.flag.p, h->stream);
+    } else {                       // NCCL: wait with async-error polling (a dead peer -> error)
+      CHASE_CUDA(cudaMemcpyAsync(h->peer.flag.p, &v, sizeof(int), cudaMemcpyHostToDevice, h->stream));
+      CHASE_NCCL(ncclAllReduce(h->peer.flag.p, h->peer.flag.p, 1, ncclInt32, ncclMax, h->world.nccl, h->stream));
+      CHASE_CUDA(cudaMemcpyAsync(&v, h->peer.flag.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+      sync_stream(h, h->stream);
+    }
     if (v != (int)st && h->err.empty()) h->err = "another rank failed with status " + std::to_string(v);
     return (chase_status)v;
   } catch (...) {
@@ -282,10 +285,20 @@ chase_status agree(chase_handle* h, chase_status st) {
   }
 }
 
+// A CUDA / NCCL failure leaves the handle unusable; its NCCL communicators are aborted so that
+// peers blocked in a collective with this rank see an error (ncclCommGetAsyncError, polled by
+// sync_stream) instead of waiting forever.
+void fail_hard(chase_handle* h) {
+  h->broken = true;
+  comm_abort(h->world);
+  comm_abort(h->rowc);
+  comm_abort(h->colc);
+}
+
+// Run f() and map exceptions to statuses.  PeerTimeout keeps the communicators usable, so its
+// status is still agreed on before the handle is marked unusable.
 template <class F>
-chase_status guarded(chase_handle* h, F&& f, bool collective = true) {
-  if (!h) return CHASE_E_USAGE;
-  if (h->broken) { h->err = "handle is unusable after an earlier CUDA/NCCL error"; return CHASE_E_CUDA; }
+chase_status run_mapped(chase_handle* h, F&& f, bool& hard, bool& soft_broken) {
   chase_status st = CHASE_OK;
   try {
     CHASE_CUDA(cudaSetDevice(h->device));
@@ -294,16 +307,52 @@ chase_status guarded(chase_handle* h, F&& f, bool collective = true) {
     h->err = e.what(); st = CHASE_E_USAGE;
   } catch (const NumericError& e) {
     h->err = e.what(); st = CHASE_E_NUMERIC;
+  } catch (const PeerTimeout& e) {
+    h->err = e.what(); st = CHASE_E_NCCL; soft_broken = true;
   } catch (const NcclError& e) {
-    h->err = e.what(); st = CHASE_E_NCCL; h->broken = true;
+    h->err = e.what(); st = CHASE_E_NCCL; hard = true;
   } catch (const CudaError& e) {
-    h->err = e.what(); st = CHASE_E_CUDA; h->broken = true;
+    h->err = e.what(); st = CHASE_E_CUDA; hard = true;
   } catch (const std::bad_alloc&) {
-    h->err = "host out of memory"; st = CHASE_E_NOMEM;
+    h->err = "out of memory (device workspace or host)"; st = CHASE_E_NOMEM;
   } catch (const std::exception& e) {
-    h->err = e.what(); st = CHASE_E_CUDA; h->broken = true;
+    h->err = e.what(); st = CHASE_E_CUDA; hard = true;
   }
-  return collective ? agree(h, st) : st;
+  return st;
+}
+
+// Collective calls: validate() runs first and touches no communicator; its status is agreed on
+// over the world, so either every rank proceeds to work() (which issues the collectives) or
+// every rank returns the same error -- a rank-local argument problem (uneven shards, ld, layout)
+// can therefore never leave the other ranks blocked inside a collective.  work()'s status is
+// agreed on as well.
+template <class V, class F>
+chase_status guarded2(chase_handle* h, V&& validate, F&& work) {
+  if (!h) return CHASE_E_USAGE;
+  if (h->broken) { h->err = "handle is unusable after an earlier CUDA/NCCL error"; return CHASE_E_CUDA; }
+  bool hard = false, soft = false;
+  chase_status st = run_mapped(h, validate, hard, soft);
+  if (hard) { fail_hard(h); return st; }
+  st = agree(h, st);
+  if (st != CHASE_OK) return st;
+  st = run_mapped(h, work, hard, soft);
+  if (hard) { fail_hard(h); return st; }
+  st = agree(h, st);
+  if (soft) h->broken = true;
+  return st;
+}
+
+// single-phase variant (local calls, and collectives with nothing rank-local to validate)
+template <class F>
+chase_status guarded(chase_handle* h, F&& f, bool collective = true) {
+  if (!h) return CHASE_E_USAGE;
+  if (h->broken) { h->err = "handle is unusable after an earlier CUDA/NCCL error"; return CHASE_E_CUDA; }
+  bool hard = false, soft = false;
+  chase_status st = run_mapped(h, f, hard, soft);
+  if (hard) { fail_hard(h); return st; }
+  if (collective) st = agree(h, st);
+  if (soft) h->broken = true;
+  return st;
 }
 
 void order_after_user(chase_handle* h) {
@@ -333,6 +382,24 @@ const char* chase_version(void) {
 
 const char* chase_last_error(const chase_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
+// Auto grid (ledger #19): r x c = world, r <= c, |r - c| minimal.
+static void auto_grid(int ws, int& r, int& c) {
+  r = 1;
+  for (int d = 1; (int64_t)d * d <= ws; ++d)
+    if (ws % d == 0) r = d;
+  c = ws / r;
+}
+
+// complex single: the TMA operand views need every shard of the grid to have q % 4 == 0 and even
+// p; decided from the global N / r / c so that every rank reaches the same answer
+static bool c64_grid_layout_ok(const Grid& g) {
+  for (int i = 0; i < g.r; ++i)
+    if (block_range(g.N, g.r, i).len % 2 != 0) return false;
+  for (int j = 0; j < g.c; ++j)
+    if (block_range(g.N, g.c, j).len % 4 != 0) return false;
+  return true;
+}
+
 chase_status chase_init(chase_handle** out, const chase_init_args* a) {
   if (!out || !a) return CHASE_E_USAGE;
   *out = nullptr;
@@ -345,19 +412,23 @@ chase_status chase_init(chase_handle** out, const chase_init_args* a) {
       throw UsageError("invalid N / nev_max / nex_max");
     int ws = std::max(1, a->world_size);
     int r = a->grid_rows, c = a->grid_cols;
-    if (r <= 0 || c <= 0) { r = 1; c = ws; }
+    if (r <= 0 || c <= 0) auto_grid(ws, r, c);
     // world_size == 1 with r*c > 1: emulated-grid mode (one shard of an r x c grid, no
     // communicators; collective sums are left to the caller).  Used by single-GPU grid tests.
     if (r * c != ws && ws != 1) throw UsageError("grid_rows * grid_cols must equal world_size");
     if (a->rank < 0 || a->rank >= r * c) throw UsageError("rank out of range");
     if (a->N < std::max(r, c)) throw UsageError("N must be >= max(r, c)");
+    if (a->colocated && ws <= 1) throw UsageError("colocated needs world_size > 1");
     h->world_size = ws;
     h->device = a->cuda_device;
+    h->colocated = a->colocated != 0;
     CHASE_CUDA(cudaSetDevice(h->device));
     int major = 0;
     CHASE_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device));
     if (major < 10) throw UsageError("this library requires an sm_100a (B200) device");
     h->grid.setup(a->N, r, c, a->rank);
+    if (h->c64() && !c64_grid_layout_ok(h->grid))
+      throw UsageError("CHASE_C64 needs every shard of the grid to have q % 4 == 0 and even p");
     CHASE_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     // NULL means the caller's work is on the legacy default stream; the library stream is
     // non-blocking, so ordering against it must be explicit (an event on cudaStreamLegacy).
@@ -366,24 +437,47 @@ chase_status chase_init(chase_handle** out, const chase_init_args* a) {
     CHASE_CUDA(cudaEventCreate(&h->ev1));
     if (ws > 1) {
       if (!a->nccl_unique_id) throw UsageError("nccl_unique_id required when world_size > 1");
-      ncclUniqueId id;
-      std::memcpy(&id, a->nccl_unique_id, sizeof(id));
-      CHASE_NCCL(ncclCommInitRank(&h->world, ws, id, a->rank));
-      CHASE_NCCL(ncclCommSplit(h->world, h->grid.i, h->grid.j, &h->rowc, nullptr));   // row comm i
-      CHASE_NCCL(ncclCommSplit(h->world, h->grid.j, h->grid.i, &h->colc, nullptr));   // column comm j
+      h->world.size = ws;
+      h->world.rank = a->rank;
+      h->rowc.size = c;                 // row comm i: colour i, key j
+      h->rowc.rank = h->grid.j;
+      h->colc.size = r;                 // column comm j: colour j, key i
+      h->colc.rank = h->grid.i;
+      if (h->colocated) {
+        // in-process rendezvous keyed by the 128-byte id (comm.h)
+        std::string key(reinterpret_cast<const char*>(a->nccl_unique_id), 128);
+        const std::string kw = key + "/world", kr = key + "/row" + std::to_string(h->grid.i),
+                          kc = key + "/col" + std::to_string(h->grid.j);
+        h->world.local = local_join(kw.data(), kw.size(), ws, a->rank);
+        h->rowc.local = local_join(kr.data(), kr.size(), c, h->grid.j);
+        h->colc.local = local_join(kc.data(), kc.size(), r, h->grid.i);
+      } else {
+        ncclUniqueId id;
+        std::memcpy(&id, a->nccl_unique_id, sizeof(id));
+        CHASE_NCCL(ncclCommInitRank(&h->world.nccl, ws, id, a->rank));
+        CHASE_NCCL(ncclCommSplit(h->world.nccl, h->grid.i, h->grid.j, &h->rowc.nccl, nullptr));   // row comm i
+        CHASE_NCCL(ncclCommSplit(h->world.nccl, h->grid.j, h->grid.i, &h->colc.nccl, nullptr));   // column comm j
+      }
       CHASE_CUDA(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
-      for (int c = 0; c < chase_handle::MAX_CHUNKS; ++c) {
-        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_gemm[c], cudaEventDisableTiming));
-        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_comm[0][c], cudaEventDisableTiming));
-        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_comm[1][c], cudaEventDisableTiming));
+      for (int k = 0; k < chase_handle::MAX_CHUNKS; ++k) {
+        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_gemm[k], cudaEventDisableTiming));
+        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_comm[0][k], cudaEventDisableTiming));
+        CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_comm[1][k], cudaEventDisableTiming));
       }
       CHASE_CUDA(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     }
     h->n_e_max = a->nev_max + a->nex_max;
     // Workspace: V, V2 (V-layout q x n_e), W, HV (W-layout p x n_e), n_e x n_e
-    // matrices.  Memory check against free device memory (P:507-531 analogue).
-    const int64_t p = h->grid.rows.len, q = h->grid.cols.len, ne = h->n_e_max;
-    const size_t need = 16 * (size_t)(2 * q * ne + 2 * p * ne + 3 * ne * ne);
+    // matrices, allocated here; the memory check (P:507-531 analogue) also counts what is
+    // allocated on first use: Lanczos Krylov basis (N x L x (m+1) + N x L), the RR eigensolver's
+    // padded n_e x n_e pair, the fused-reduce staging buffer (grids), and for complex single the
+    // shard's 3xTF32 lo part and the operand formats.
+    const int64_t p = h->grid.rows.len, q = h->grid.cols.len, ne = h->n_e_max, N = a->N;
+    const int64_t np = (ne + 63) / 64 * 64;
+    size_t need = 16 * (size_t)(2 * q * ne + 2 * p * ne + 3 * ne * ne);
+    need += 16 * (size_t)N * 4 * 27 + 2 * 16 * (size_t)np * np;
+    if (ws > 1) need += 16 * (size_t)std::max(p, q) * ne;
+    if (h->c64()) need += 8 * (size_t)p * q + 16 * (size_t)q * ne + 32 * (size_t)p * ne;
     size_t fre = 0, tot = 0;
     CHASE_CUDA(cudaMemGetInfo(&fre, &tot));
     if (need > fre) throw std::bad_alloc();
@@ -431,6 +525,8 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     else if (k == "mixed_filter") h->opt.mixed_filter = v;
     else if (k == "fused_reduce") h->opt.fused_reduce = v != 0.0;
     else if (k == "fused_reduce_c64") h->opt.fused_reduce_c64 = v != 0.0;
+    else if (k == "peer_timeout") { if (!(v > 0)) throw UsageError("peer_timeout > 0"); h->opt.peer_timeout = v; }
+    else if (k == "comm_timeout") { if (v < 0) throw UsageError("comm_timeout >= 0"); h->opt.comm_timeout = v; }
     else throw UsageError("unknown option " + k);
     return CHASE_OK;
   }, false);
@@ -449,18 +545,22 @@ chase_status chase_local_layout(const chase_handle* h, int64_t* row0, int64_t* p
 chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H, int64_t ldh,
                              const void* X, int64_t ldx, void* Y, int64_t ldy, int32_t ncols,
                              double alpha, double beta, double gamma) {
-  return guarded(h, [&]() {
+  return guarded2(h, [&]() {
     const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
     if (dir != 0 && dir != 1) throw UsageError("dir must be 0 or 1");
     if (ncols == 0) return CHASE_OK;   // empty block: no-op, pointers may be NULL
     if (!H || !X || !Y || ncols < 0 || ldh < p) throw UsageError("bad pointers / sizes");
     if (ldx < (dir == 0 ? q : p) || ldy < (dir == 0 ? p : q)) throw UsageError("bad leading dimension");
+    if (h->c64()) c64_check_call(h, H, ldh, ncols);
+    return CHASE_OK;
+  }, [&]() {
+    if (ncols == 0) return CHASE_OK;
     order_after_user(h);
     if (h->c64())
       c64_hemm_step(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma);
     else
       hemm_step(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma);
-    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    sync_stream(h, h->stream);
     return CHASE_OK;
   });
 }
@@ -468,14 +568,22 @@ chase_status chase_hemm_step(chase_handle* h, int32_t dir, const void* H, int64_
 chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv,
                           void* W, int64_t ldw, int32_t ncols, const int32_t* degrees,
                           double b_sup, double mu_1, double mu_ne, int64_t* matvecs) {
-  return guarded(h, [&]() {
+  if (matvecs) *matvecs = 0;
+  return guarded2(h, [&]() {
     const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
-    if (ncols == 0) {                  // empty block: no-op, pointers may be NULL
-      if (matvecs) *matvecs = 0;
-      return CHASE_OK;
-    }
+    if (ncols == 0) return CHASE_OK;   // empty block: no-op, pointers may be NULL
     if (!H || !V || !W || ncols < 0 || !degrees) throw UsageError("bad pointers");
     if (ldh < p || ldv < q || ldw < p) throw UsageError("bad leading dimension");
+    for (int a = 0; a < ncols; ++a) {
+      if (degrees[a] < 0 || (degrees[a] & 1)) throw UsageError("filter degrees must be even and >= 0");
+      if (a > 0 && degrees[a] < degrees[a - 1]) throw UsageError("filter degrees must be sorted ascending");
+    }
+    if (degrees[ncols - 1] > 0 && !(b_sup > mu_ne)) throw UsageError("filter interval is empty (b_sup <= mu_ne)");
+    if (h->c64()) c64_check_call(h, H, ldh, ncols);
+    return CHASE_OK;
+  }, [&]() {
+    if (ncols == 0) return CHASE_OK;
+    const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
     order_after_user(h);
     const Grid& g = h->grid;
     // f1 runs on the library's V / W workspace (the peers' replicas): stage the caller's block
@@ -495,7 +603,7 @@ chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, 
     } else {
       mv = filter(h, H, ldh, V, ldv, W, ldw, ncols, degrees, b_sup, mu_1, mu_ne);
     }
-    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    sync_stream(h, h->stream);
     if (matvecs) *matvecs = mv;
     return CHASE_OK;
   });
@@ -503,8 +611,10 @@ chase_status chase_filter(chase_handle* h, const void* H, int64_t ldh, void* V, 
 
 chase_status chase_lanczos(chase_handle* h, const void* H, int64_t ldh, int32_t n_e, double* b_sup,
                            double* mu_1, double* mu_ne, double* nu) {
-  return guarded(h, [&]() {
+  return guarded2(h, [&]() {
     if (!H || ldh < h->grid.rows.len || n_e <= 0 || n_e > h->grid.N) throw UsageError("bad arguments");
+    return CHASE_OK;
+  }, [&]() {
     order_after_user(h);
     LanczosOut o = lanczos(h, H, ldh, n_e);
     if (b_sup) *b_sup = o.b_sup;
@@ -522,7 +632,7 @@ chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t c
     if (!V || ldv < h->grid.cols.len || ncols < 0) throw UsageError("bad arguments");
     order_after_user(h);
     random_block(h, V, ldv, h->grid.cols.len, h->grid.cols.start, col0, ncols, seed, stream, h->c64());
-    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    sync_stream(h, h->stream);
     return CHASE_OK;
   }, false);
 }
@@ -530,15 +640,21 @@ chase_status chase_random_block(chase_handle* h, void* V, int64_t ldv, int32_t c
 chase_status chase_solve(chase_handle* h, const void* H, int64_t ldh, int64_t N, int32_t nev,
                          int32_t nex, int32_t deg, double tol, double* ritz_values,
                          void* ritz_vectors, int64_t ldv, chase_report* report) {
-  return guarded(h, [&]() {
+  return guarded2(h, [&]() {
     if (N != h->grid.N) throw UsageError("N differs from chase_init");
     if (!(nev > 0 && nex > 0 && (int64_t)nev + nex <= N && tol > 0 && deg >= 1))
       throw UsageError("invalid nev / nex / tol / deg (S:407)");
     if (nev + nex > h->n_e_max) throw UsageError("nev + nex exceeds nev_max + nex_max of chase_init");
     if (!H || ldh < h->grid.rows.len || !ritz_values || !ritz_vectors || ldv < h->grid.cols.len)
       throw UsageError("bad pointers / leading dimensions");
+    if (h->c64()) c64_check_call(h, H, ldh, nev + nex);
+    if (h->dtype == CHASE_C128 && h->opt.mixed_filter > 0.0) {
+      if (!c64_grid_layout_ok(h->grid))
+        throw UsageError("mixed_filter needs every shard of the grid to have q % 4 == 0 and even p");
+    }
+    return CHASE_OK;
+  }, [&]() {
     order_after_user(h);
-    if (h->c64()) c64_hlo(h, H, ldh);             // validates the c64 shard layout up front
     return solve(h, H, ldh, nev, nex, deg, tol, ritz_values, ritz_vectors, ldv, report);
   });
 }
@@ -548,8 +664,8 @@ chase_status chase_heev(chase_handle* h, void* G, int64_t ld, int32_t n, double*
   return guarded(h, [&]() {
     if (!G || !theta || !Z || n <= 0 || ld < n || ldz < n) throw UsageError("bad arguments");
     order_after_user(h);
-    const int sw = heev_jacobi(G, ld, n, theta, Z, ldz, h->stream);
-    CHASE_CUDA(cudaStreamSynchronize(h->stream));
+    const int sw = heev_jacobi(G, ld, n, theta, Z, ldz, h->stream, &h->jacobi);
+    sync_stream(h, h->stream);
     if (sweeps) *sweeps = sw;
     return CHASE_OK;
   }, false);
@@ -563,9 +679,11 @@ chase_status chase_finalize(chase_handle* h) {
   for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo,
                          &h->c64v, &h->c64w, &h->H32})
     b->release();
-  if (h->rowc) ncclCommDestroy(h->rowc);
-  if (h->colc) ncclCommDestroy(h->colc);
-  if (h->world) ncclCommDestroy(h->world);
+  heev_work_release(h->jacobi);
+  h->jacobi = nullptr;
+  comm_destroy(h->rowc);
+  comm_destroy(h->colc);
+  comm_destroy(h->world);
   if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
   for (int c = 0; c < chase_handle::MAX_CHUNKS; ++c) {
     if (h->ev_gemm[c]) cudaEventDestroy(h->ev_gemm[c]);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <new>
 #include <stdexcept>
 #include "common.cuh"
 #include <string>
@@ -9,6 +10,8 @@
 #include "../../include/chase.h"
 #include "grid.h"
 #include "zgemm.h"
+#include "comm.h"
+#include "linalg.h"
 
 namespace chase {
 
@@ -20,6 +23,11 @@ struct UsageError : std::runtime_error {
 };
 struct NumericError : std::runtime_error {
   using std::runtime_error::runtime_error;
+};
+// a fused-reduce peer stopped arriving: the communicators themselves are intact, so the status is
+// still agreed on over the world before the handle is marked unusable
+struct PeerTimeout : NcclError {
+  using NcclError::NcclError;
 };
 
 #define CHASE_NCCL(call)                                                                        \
@@ -38,7 +46,13 @@ struct DBuf {
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
-    CHASE_CUDA(cudaMalloc(&p, b));
+    const cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaErrorMemoryAllocation) {          // surfaces as CHASE_E_NOMEM, handle stays usable
+      cudaGetLastError();
+      p = nullptr;
+      throw std::bad_alloc();
+    }
+    CHASE_CUDA(e);
     bytes = b;
   }
   void release() {
@@ -62,6 +76,8 @@ struct Options {
   double mixed_filter = 0.0;  // f4: complex-single filter while all active residuals exceed this
   bool fused_reduce = true;   // f1: filter steps all-reduce inside the GEMM over peer memory
   bool fused_reduce_c64 = false;  // f1 for the complex-single filter (measured slower than NCCL + rebuild)
+  double peer_timeout = 120.0;    // f1: seconds a rank waits for its peers' tiles before failing
+  double comm_timeout = 0.0;      // host waits poll ncclCommGetAsyncError; > 0: also fail after this many s
 };
 
 }  // namespace chase
@@ -77,7 +93,8 @@ struct chase_handle {
   int world_size = 1;
   cudaStream_t stream = nullptr;       // library stream (all kernels, NCCL)
   cudaStream_t user_stream = nullptr;  // caller stream to order against
-  ncclComm_t world = nullptr, rowc = nullptr, colc = nullptr;
+  chase::Comm world, rowc, colc;       // NCCL or co-located transport (comm.h)
+  bool colocated = false;              // ranks are threads of this process (comm.h)
   chase::Options opt;
   int n_e_max = 0;
   // workspace
@@ -89,6 +106,7 @@ struct chase_handle {
   int64_t h32_ld = 0;
   const void* hlo_src = nullptr;
   int64_t hlo_ld = 0;
+  chase::JacobiWork* jacobi = nullptr;  // RR eigensolver workspace (linalg.h)
   std::vector<double> host_scratch;
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -100,9 +118,10 @@ struct chase_handle {
   // f1: fused all-reduce over peer memory (peer.cu)
   struct Peer {
     bool ready = false, failed = false;
-    chase::DBuf stage, ctr, flag;
+    chase::DBuf stage, ctr, flag, xbuf;
     unsigned* done_local = nullptr;
-    unsigned* err = nullptr;
+    unsigned* err = nullptr;              // device view of err_host (mapped pinned memory)
+    volatile unsigned* err_host = nullptr;  // set by the wait kernel on timeout; read between steps
     unsigned expected = 0;
     chase::PeerRed row, col;
     bool c64_ready = false;
@@ -123,9 +142,8 @@ void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void*
 int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, void* W,
                int64_t ldw, int ncols, const int* degrees, double b_sup, double mu_1, double mu_ne);
 // in-place sum over a communicator of a column block (rows x ncols, ld)
-void allreduce_block(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows,
-                     int64_t ld, int ncols);
-void allreduce_doubles(chase_handle* h, ncclComm_t comm, int comm_size, double* x, size_t n);
+void allreduce_block(chase_handle* h, const Comm& comm, void* Y, int64_t rows, int64_t ld, int ncols);
+void allreduce_doubles(chase_handle* h, const Comm& comm, double* x, size_t n);
 
 struct LanczosOut {
   double b_sup, mu_1, mu_ne, nu;
@@ -136,13 +154,15 @@ void random_block(chase_handle* h, void* V, int64_t ldv, int64_t rows, int64_t g
                   int ncols, uint64_t seed, uint32_t stream_id, bool c64_out = false);
 
 // complex-single (c64) path: tcgen05 3xTF32 fused step and filter (c64.cu)
-void allreduce_c64(chase_handle* h, ncclComm_t comm, int comm_size, void* Y, int64_t rows, int64_t ld, int ncols);
+void allreduce_c64(chase_handle* h, const Comm& comm, void* Y, int64_t rows, int64_t ld, int ncols);
 void c64_hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx, void* Y,
                    int64_t ldy, int ncols, double alpha, double beta, double gamma);
 int64_t c64_filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv, int ncols, const int* degrees,
                    double b_sup, double mu_1, double mu_ne);
 // f4: complex64 shadow (ld p) of a complex128 shard, rebuilt when H / ldh change
 const void* c64_shadow(chase_handle* h, const void* H, int64_t ldh);
+// rank-local argument checks of a complex-single call (alignment, ld, width); throws UsageError
+void c64_check_call(chase_handle* h, const void* H, int64_t ldh, int ncols);
 // H_lo of the shard (validates the c64 layout; recomputed when H / ldh change)
 const void* c64_hlo(chase_handle* h, const void* H, int64_t ldh);
 // mixed solve (c64 shard, complex128 iteration): filter / HX on complex128 blocks, and conversions
@@ -160,6 +180,15 @@ const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y);
 void peer_wait(chase_handle* h, int tiles);
 void peer_check(chase_handle* h);
 void peer_release(chase_handle* h);
+// tile count of one fused step fits the arrival counters (else the step all-reduces with NCCL)
+bool peer_tiles_fit(int tiles);
+// barrier over the world before a fused filter (ranks enter within the peer timeout of each other)
+void peer_enter(chase_handle* h);
+// throws PeerTimeout if a wait kernel has timed out (host read of mapped memory, no sync)
+void peer_poll(chase_handle* h);
+// synchronise the library stream, polling the communicators' asynchronous errors (and the
+// comm_timeout option) while waiting
+void sync_stream(chase_handle* h, cudaStream_t st);
 
 chase_status solve(chase_handle* h, const void* H, int64_t ldh, int nev, int nex, int deg,
                    double tol, double* ritz_values, void* ritz_vectors, int64_t ldv,

@@ -371,7 +371,9 @@ __global__ void k_extract(const double2* A, const double2* Zp, int np, int n, co
   }
 }
 
-struct Work {
+}  // namespace
+
+struct JacobiWork {
   void* A = nullptr; void* Zp = nullptr; void* U = nullptr; int* pairs = nullptr; int* order = nullptr;
   double* part = nullptr;
   size_t np = 0, b = 0;
@@ -392,17 +394,20 @@ struct Work {
     A = Zp = U = nullptr; pairs = order = nullptr; part = nullptr; np = b = 0;
   }
 };
-Work g_works[64];   // per device; one solve at a time per device (the library is single-threaded per handle)
-}  // namespace
 
-int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz, cudaStream_t st) {
+void heev_work_release(JacobiWork* w) {
+  if (!w) return;
+  w->release();
+  delete w;
+}
+
+int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz, cudaStream_t st, JacobiWork** work) {
   if (n <= 0) return 0;
   const int np = ceil_div(n, S) * S;
   const int b = np / S;           // pairs per round; 2b blocks of W
   const int nblocks = 2 * b;
-  int dev = 0;
-  CHASE_CUDA(cudaGetDevice(&dev));
-  Work& g_work = g_works[dev & 63];
+  if (!*work) *work = new JacobiWork();
+  JacobiWork& g_work = **work;
   g_work.ensure(np, st);
   static unsigned long long attr = 0;
   const int smem = (int)(2 * sizeof(double2) * S * LD);

@@ -183,7 +183,7 @@ static LanczosOut lanczos_t(chase_handle* h, const void* H, int64_t ldh, int n_e
       d.alpha = hsign; d.beta = 0.0;
       gemm(h, d);
     }
-    allreduce_doubles(h, h->world, h->world_size, reinterpret_cast<double*>(F), SC<T>::ND * (size_t)N * L);
+    allreduce_doubles(h, h->world, reinterpret_cast<double*>(F), SC<T>::ND * (size_t)N * L);
     // two classical Gram-Schmidt passes against Q_0..Q_j (full reorthogonalisation); the first
     // pass's coefficient on Q_j is alpha_j = Re(q_j^H H q_j)
     dots_into(Q, j + 1, F, hc);

@@ -18,7 +18,10 @@ void trinv_upper(const void* R, int64_t ldr, void* X, int64_t ldx, void* T, int 
 // (64 x 64 subproblems solved in one CTA each, updates as 64 x 64 complex tile products).
 // G: n x n (ld) device, destroyed.  theta: device n doubles ascending.  Z: device n x n (ldz).
 // Returns the number of sweeps; throws NumericError if not converged.
+// `work`: the caller's workspace slot (a handle owns one; allocated / grown on first use, freed by
+// heev_work_release), so concurrent handles on one device never share buffers.
 struct JacobiWork;
-int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz, cudaStream_t st);
+int heev_jacobi(void* G, int64_t ld, int n, double* theta, void* Z, int64_t ldz, cudaStream_t st, JacobiWork** work);
+void heev_work_release(JacobiWork* work);
 
 }  // namespace chase

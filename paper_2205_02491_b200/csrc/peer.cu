@@ -8,7 +8,10 @@
 // NVLink5 / NVSwitch carries the peer loads and stores issued by the GEMM epilogue
 // (zgemm3m.cuh).  After each fused step a one-thread kernel waits on the local completion
 // counter, which the reducers bump once per tile, so the next step reads a complete replica.
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -30,7 +33,8 @@ __global__ void k_wait_done(const unsigned* done, unsigned target, unsigned* err
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (t - t0 > timeout_ns) {
-      atomicExch(err, 1u);
+      *reinterpret_cast<volatile unsigned*>(err) = 1u;
+      __threadfence_system();
       return;
     }
     __nanosleep(200);
@@ -39,23 +43,19 @@ __global__ void k_wait_done(const unsigned* done, unsigned target, unsigned* err
 
 struct Handles {
   cudaIpcMemHandle_t stage, vec, ctr;
+  void *raw_stage, *raw_vec, *raw_ctr;     // co-located ranks: the device pointers themselves
 };
 
-// all-gather `mine` over `comm` (size n) -> out[n]
-void gather_handles(chase_handle* h, ncclComm_t comm, int n, const Handles& mine, std::vector<Handles>& out) {
-  out.assign(n, Handles{});
-  void* d = nullptr;
-  CHASE_CUDA(cudaMalloc(&d, sizeof(Handles) * (n + 1)));
-  CHASE_CUDA(cudaMemcpyAsync(d, &mine, sizeof(Handles), cudaMemcpyHostToDevice, h->stream));
-  CHASE_NCCL(ncclAllGather(d, reinterpret_cast<char*>(d) + sizeof(Handles), sizeof(Handles), ncclUint8, comm,
-                           h->stream));
-  CHASE_CUDA(cudaMemcpyAsync(out.data(), reinterpret_cast<char*>(d) + sizeof(Handles), sizeof(Handles) * n,
-                             cudaMemcpyDeviceToHost, h->stream));
-  CHASE_CUDA(cudaStreamSynchronize(h->stream));
-  cudaFree(d);
+// all-gather `mine` over `comm` -> out[comm.size]
+template <class T>
+void gather(chase_handle* h, const Comm& comm, const T& mine, std::vector<T>& out) {
+  out.assign(comm.size, T{});
+  h->peer.xbuf.alloc(sizeof(T) * (comm.size + 1));
+  comm_allgather_host(comm, &mine, sizeof(T), out.data(), h->peer.xbuf.p, h->stream);
 }
 
-void* open_peer(chase_handle* h, const cudaIpcMemHandle_t& hd) {
+void* open_peer(chase_handle* h, const cudaIpcMemHandle_t& hd, void* raw) {
+  if (h->colocated) return raw;            // same process (and device): no IPC mapping needed
   void* p = nullptr;
   CHASE_CUDA(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
   h->peer.opened.push_back(p);
@@ -66,12 +66,7 @@ void* open_peer(chase_handle* h, const cudaIpcMemHandle_t& hd) {
 // every rank's local success flag, min over the world (collective); false if any rank failed
 static bool all_ok(chase_handle* h, bool ok) {
   h->peer.flag.alloc(sizeof(int));
-  int v = ok ? 1 : 0;
-  CHASE_CUDA(cudaMemcpyAsync(h->peer.flag.p, &v, sizeof(int), cudaMemcpyHostToDevice, h->stream));
-  CHASE_NCCL(ncclAllReduce(h->peer.flag.p, h->peer.flag.p, 1, ncclInt32, ncclMin, h->world, h->stream));
-  CHASE_CUDA(cudaMemcpyAsync(&v, h->peer.flag.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CHASE_CUDA(cudaStreamSynchronize(h->stream));
-  return v != 0;
+  return comm_allreduce_int(h->world, ok ? 1 : 0, Op::Min, h->peer.flag.p, h->stream) != 0;
 }
 
 static void give_up(chase_handle* h, const char* why) {
@@ -85,7 +80,7 @@ static void give_up(chase_handle* h, const char* why) {
 static bool peer_base_ready(chase_handle* h) {
   const Grid& g = h->grid;
   if (h->peer.failed || !h->opt.fused_reduce) return false;
-  if (h->world_size <= 1 || !h->world || (g.r <= 1 && g.c <= 1)) return false;
+  if (h->world_size <= 1 || !h->world.active() || (g.r <= 1 && g.c <= 1)) return false;
   if (g.r > kMaxPeers || g.c > kMaxPeers) return false;
   if (h->peer.ready) return true;
   // ---- collective setup (every rank of the grid reaches this point with the same options).  Local
@@ -101,19 +96,33 @@ static bool peer_base_ready(chase_handle* h) {
     CHASE_CUDA(cudaMemsetAsync(h->peer.ctr.p, 0, h->peer.ctr.bytes, h->stream));
     base = h->peer.ctr.as<unsigned>();
     h->peer.done_local = base + 2 * kCtrPerComm;
-    h->peer.err = base + 2 * kCtrPerComm + 32;
-    CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.stage, h->peer.stage.p));
-    CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.ctr, h->peer.ctr.p));
+    if (!h->peer.err_host) {
+      unsigned* hp = nullptr;
+      CHASE_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hp), 64, cudaHostAllocMapped));
+      *hp = 0;
+      h->peer.err_host = hp;
+      CHASE_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->peer.err), hp, 0));
+    }
+    if (!h->colocated) {
+      CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.stage, h->peer.stage.p));
+      CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.ctr, h->peer.ctr.p));
+    }
+    row_mine.raw_stage = h->peer.stage.p;
+    row_mine.raw_ctr = h->peer.ctr.p;
     col_mine = row_mine;
-    CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.vec, h->W.p));      // row comm sums W-layout blocks
-    CHASE_CUDA(cudaIpcGetMemHandle(&col_mine.vec, h->V.p));      // column comm sums V-layout blocks
+    row_mine.raw_vec = h->W.p;                                   // row comm sums W-layout blocks
+    col_mine.raw_vec = h->V.p;                                   // column comm sums V-layout blocks
+    if (!h->colocated) {
+      CHASE_CUDA(cudaIpcGetMemHandle(&row_mine.vec, h->W.p));
+      CHASE_CUDA(cudaIpcGetMemHandle(&col_mine.vec, h->V.p));
+    }
   } catch (const std::exception&) {
     cudaGetLastError();
     ok = false;
   }
   std::vector<Handles> rows_h, cols_h;
-  if (g.c > 1) gather_handles(h, h->rowc, g.c, row_mine, rows_h);
-  if (g.r > 1) gather_handles(h, h->colc, g.r, col_mine, cols_h);
+  if (g.c > 1) gather(h, h->rowc, row_mine, rows_h);
+  if (g.r > 1) gather(h, h->colc, col_mine, cols_h);
   if (!all_ok(h, ok)) {
     give_up(h, "setup");
     return false;
@@ -128,9 +137,9 @@ static bool peer_base_ready(chase_handle* h) {
         pr.out[r] = reinterpret_cast<double2*>(own_vec);
         ctrs[r] = base;
       } else {
-        pr.stage[r] = reinterpret_cast<double2*>(open_peer(h, hs[r].stage));
-        pr.out[r] = reinterpret_cast<double2*>(open_peer(h, hs[r].vec));
-        ctrs[r] = reinterpret_cast<unsigned*>(open_peer(h, hs[r].ctr));
+        pr.stage[r] = reinterpret_cast<double2*>(open_peer(h, hs[r].stage, hs[r].raw_stage));
+        pr.out[r] = reinterpret_cast<double2*>(open_peer(h, hs[r].vec, hs[r].raw_vec));
+        ctrs[r] = reinterpret_cast<unsigned*>(open_peer(h, hs[r].ctr, hs[r].raw_ctr));
       }
       pr.done[r] = ctrs[r] + 2 * kCtrPerComm;
     }
@@ -171,23 +180,20 @@ bool peer_c64_ready(chase_handle* h) {
   if (h->peer.c64_ready) return true;
   const Grid& g = h->grid;
   if (!h->c64v.p || !h->c64w.p) throw std::logic_error("peer_c64_ready before the c64 formats exist");
-  struct H2 { cudaIpcMemHandle_t buf; } mine_r{}, mine_c{};
-  CHASE_CUDA(cudaIpcGetMemHandle(&mine_r.buf, h->c64w.p));
-  CHASE_CUDA(cudaIpcGetMemHandle(&mine_c.buf, h->c64v.p));
+  struct H2 { cudaIpcMemHandle_t buf; void* raw; } mine_r{}, mine_c{};
+  if (!h->colocated) {
+    CHASE_CUDA(cudaIpcGetMemHandle(&mine_r.buf, h->c64w.p));
+    CHASE_CUDA(cudaIpcGetMemHandle(&mine_c.buf, h->c64v.p));
+  }
+  mine_r.raw = h->c64w.p;
+  mine_c.raw = h->c64v.p;
   bool ok = true;
-  auto xchg = [&](ncclComm_t comm, int n, int me, const H2& mine, float** out, void* own) {
-    std::vector<H2> all(n);
-    void* d = nullptr;
-    CHASE_CUDA(cudaMalloc(&d, sizeof(H2) * (n + 1)));
-    CHASE_CUDA(cudaMemcpyAsync(d, &mine, sizeof(H2), cudaMemcpyHostToDevice, h->stream));
-    CHASE_NCCL(ncclAllGather(d, reinterpret_cast<char*>(d) + sizeof(H2), sizeof(H2), ncclUint8, comm, h->stream));
-    CHASE_CUDA(cudaMemcpyAsync(all.data(), reinterpret_cast<char*>(d) + sizeof(H2), sizeof(H2) * n,
-                               cudaMemcpyDeviceToHost, h->stream));
-    CHASE_CUDA(cudaStreamSynchronize(h->stream));
-    cudaFree(d);
+  auto xchg = [&](const Comm& comm, int n, int me, const H2& mine, float** out, void* own) {
+    std::vector<H2> all;
+    gather(h, comm, mine, all);
     try {
       for (int r = 0; r < n; ++r)
-        out[r] = r == me ? reinterpret_cast<float*>(own) : reinterpret_cast<float*>(open_peer(h, all[r].buf));
+        out[r] = r == me ? reinterpret_cast<float*>(own) : reinterpret_cast<float*>(open_peer(h, all[r].buf, all[r].raw));
     } catch (const std::exception&) {
       cudaGetLastError();
       ok = false;
@@ -214,21 +220,39 @@ const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y) {
   return &pr;
 }
 
+bool peer_tiles_fit(int tiles) { return tiles >= 0 && tiles <= kCtrPerComm; }
+
+void peer_enter(chase_handle* h) {
+  h->peer.flag.alloc(sizeof(int));
+  comm_allreduce_int(h->world, 1, Op::Min, h->peer.flag.p, h->stream);
+}
+
+void peer_poll(chase_handle* h) {
+  if (h->peer.err_host && *h->peer.err_host) {
+    h->peer.failed = true;
+    throw PeerTimeout("fused peer all-reduce timed out (a peer stopped arriving)");
+  }
+}
+
 void peer_wait(chase_handle* h, int tiles) {
   h->peer.expected += (unsigned)tiles;
-  k_wait_done<<<1, 1, 0, h->stream>>>(h->peer.done_local, h->peer.expected, h->peer.err, 20ull * 1000000000ull);
+  if (h->colocated) {
+    // co-located ranks share this process (and usually the device): no kernel may spin on a peer
+    // whose launch depends on a host thread, so completion is ordered by events -- every rank's
+    // fused GEMM of this step (hence every last-arriver reduction) precedes the next step.  The
+    // wait kernel below then only checks the counter protocol (it returns at once when it holds).
+    comm_event_barrier(h->world, h->stream);
+  }
+  const double tmo = std::max(0.001, h->opt.peer_timeout);
+  k_wait_done<<<1, 1, 0, h->stream>>>(h->peer.done_local, h->peer.expected, h->peer.err,
+                                      (unsigned long long)(tmo * 1e9));
   CHASE_CHECK_LAUNCH();
 }
 
 void peer_check(chase_handle* h) {
   if (!h->peer.ready) return;
-  unsigned e = 0;
-  CHASE_CUDA(cudaMemcpyAsync(&e, h->peer.err, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
-  CHASE_CUDA(cudaStreamSynchronize(h->stream));
-  if (e) {
-    h->peer.failed = true;
-    throw NcclError("fused peer all-reduce timed out (a peer stopped arriving)");
-  }
+  sync_stream(h, h->stream);
+  peer_poll(h);
 }
 
 void peer_release(chase_handle* h) {
@@ -237,8 +261,34 @@ void peer_release(chase_handle* h) {
   h->peer.stage.release();
   h->peer.ctr.release();
   h->peer.flag.release();
+  h->peer.xbuf.release();
+  if (h->peer.err_host) cudaFreeHost(const_cast<unsigned*>(h->peer.err_host));
+  h->peer.err_host = nullptr;
+  h->peer.err = nullptr;
   h->peer.ready = false;
   h->peer.c64_ready = false;
+}
+
+void sync_stream(chase_handle* h, cudaStream_t st) {
+  const bool poll = h->world.nccl || h->rowc.nccl || h->colc.nccl;
+  if (!poll && h->opt.comm_timeout <= 0.0) {
+    CHASE_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  unsigned spins = 0;
+  while (true) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) CHASE_CUDA(e);
+    comm_check_async(h->world);
+    comm_check_async(h->rowc);
+    comm_check_async(h->colc);
+    if (h->opt.comm_timeout > 0.0 &&
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > h->opt.comm_timeout)
+      throw NcclError("library stream did not complete within comm_timeout (a peer may have failed)");
+    if (++spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 }  // namespace chase

@@ -89,19 +89,19 @@ bool chol_and_inverse<double>(void* G, void* G2, void* Z, int n, int* d_info, cu
 
 // Rayleigh-Ritz eigensolver: G (n x n Hermitian / symmetric, destroyed) -> theta, eigenvectors in *Zout
 template <class T>
-void rr_eig(void* G, void* G2, void* Z, int n, double* theta, cudaStream_t st, void** Zout);
+void rr_eig(chase_handle* h, void* G, void* G2, void* Z, int n, double* theta, cudaStream_t st, void** Zout);
 
 template <>
-void rr_eig<double2>(void* G, void*, void* Z, int n, double* theta, cudaStream_t st, void** Zout) {
-  heev_jacobi(G, n, n, theta, Z, n, st);
+void rr_eig<double2>(chase_handle* h, void* G, void*, void* Z, int n, double* theta, cudaStream_t st, void** Zout) {
+  heev_jacobi(G, n, n, theta, Z, n, st, &h->jacobi);
   *Zout = Z;
 }
 
 template <>
-void rr_eig<double>(void* G, void* G2, void* Z, int n, double* theta, cudaStream_t st, void** Zout) {
+void rr_eig<double>(chase_handle* h, void* G, void* G2, void* Z, int n, double* theta, cudaStream_t st, void** Zout) {
   double2* Gc = reinterpret_cast<double2*>(G2);
   real_to_complex(Gc, n, reinterpret_cast<const double*>(G), n, n, n, st);
-  heev_jacobi(Gc, n, n, theta, Z, n, st);                       // real rotations: Z stays real
+  heev_jacobi(Gc, n, n, theta, Z, n, st, &h->jacobi);           // real rotations: Z stays real
   complex_to_real(reinterpret_cast<double*>(G), n, reinterpret_cast<const double2*>(Z), n, n, n, st);
   *Zout = G;
 }
@@ -207,7 +207,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
       d.M = locked; d.N = n_act; d.K = (int)q; d.conjA = true;
       d.A = V; d.lda = q; d.B = Va; d.ldb = q; d.C = G2; d.ldc = locked;
       gemm(h, d);
-      allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G2), ND * (size_t)locked * n_act);
+      allreduce_doubles(h, h->rowc, reinterpret_cast<double*>(G2), ND * (size_t)locked * n_act);
       ZgemmDesc e;                                  // Va -= Y T
       e.use3m = h->opt.gemm3m;
       e.M = (int)q; e.N = n_act; e.K = locked;
@@ -224,7 +224,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
         d.upper_only = true;                        // Cholesky reads the upper triangle only
         d.A = Va; d.lda = q; d.B = Va; d.ldb = q; d.C = G; d.ldc = n_act;
         gemm(h, d);
-        allreduce_doubles(h, h->rowc, g.c, reinterpret_cast<double*>(G), ND * (size_t)n_act * n_act);
+        allreduce_doubles(h, h->rowc, reinterpret_cast<double*>(G), ND * (size_t)n_act * n_act);
       };
       gram();
       void* Rinv = nullptr;
@@ -235,7 +235,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
         std::vector<T> dg(n_act);
         CHASE_CUDA(cudaMemcpy2DAsync(dg.data(), sizeof(T), G, sizeof(T) * (n_act + 1), sizeof(T), n_act,
                                      cudaMemcpyDeviceToHost, st));
-        CHASE_CUDA(cudaStreamSynchronize(st));
+        sync_stream(h, st);
         double trace = 0.0;
         for (auto& v : dg) trace += SC<T>::re(v);
         const double s = 11.0 * ((double)g.N * n_act + (double)n_act * (n_act + 1)) * 1.1102230246251565e-16 * trace;
@@ -275,10 +275,10 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     } else {
       zero2d<T>(G, n_act, n_act, n_act, st);
     }
-    allreduce_doubles(h, h->world, h->world_size, reinterpret_cast<double*>(G), ND * (size_t)n_act * n_act);
+    allreduce_doubles(h, h->world, reinterpret_cast<double*>(G), ND * (size_t)n_act * n_act);
     hermitize<T>(G, n_act, n_act, st);
     void* Zr = nullptr;
-    rr_eig<T>(G, G2, Z, n_act, d_theta, st, &Zr);
+    rr_eig<T>(h, G, G2, Z, n_act, d_theta, st, &Zr);
     {
       ZgemmDesc d;                                  // V <- Q Z
       d.use3m = h->opt.gemm3m;
@@ -300,11 +300,11 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
       resid_norms2<T>(Wa + (I.start - r0), p, Va + (I.start - c0), q, d_theta, I.len, n_act, d_res2, part, st);
     else
       CHASE_CUDA(cudaMemsetAsync(d_res2, 0, sizeof(double) * n_act, st));
-    allreduce_doubles(h, h->world, h->world_size, d_res2, n_act);
+    allreduce_doubles(h, h->world, d_res2, n_act);
     t_res.stop(st);
     CHASE_CUDA(cudaMemcpyAsync(th_h.data(), d_theta, sizeof(double) * n_act, cudaMemcpyDeviceToHost, st));
     CHASE_CUDA(cudaMemcpyAsync(r2_h.data(), d_res2, sizeof(double) * n_act, cudaMemcpyDeviceToHost, st));
-    CHASE_CUDA(cudaStreamSynchronize(st));
+    sync_stream(h, st);
     const double f0 = t_f.total_ms, q0 = t_qr.total_ms, r0_ = t_rr.total_ms, s0 = t_res.total_ms;
     t_f.collect(); t_qr.collect(); t_rr.collect(); t_res.collect();
     for (int a = 0; a < n_act; ++a) {
@@ -354,7 +354,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     CHASE_CUDA(cudaMemcpyAsync(d_perm, perm.data(), sizeof(int) * na, cudaMemcpyHostToDevice, st));
     permute_cols<T>(V2, q, V + (int64_t)locked * q, q, q, d_perm, na, st);
     copy2d<T>(V + (int64_t)locked * q, q, V2, q, q, na, st);
-    CHASE_CUDA(cudaStreamSynchronize(st));   // perm (host) goes out of scope
+    sync_stream(h, st);   // perm (host) goes out of scope
   }
 
   // ---- results: nev smallest locked Ritz pairs, ascending
@@ -378,7 +378,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     permute_cols<T>(ritz_vectors, ldv_out, V, q, q, d_perm, nev, st);
   }
   t_all.stop(st);
-  CHASE_CUDA(cudaStreamSynchronize(st));
+  sync_stream(h, st);
   t_all.collect();
   t_lz.collect();
   if (rep) {

@@ -7,6 +7,7 @@ every data-path collective is the library's own NCCL call inside libchase_b200.s
   shard(N, grid, rank) (row0, p, col0, q) of rank = i + j*r
   broadcast_nccl_id    rank 0 draws the ncclUniqueId through the library, everyone receives it
   max_over_ranks(x)    float max over the process group (timing rule: max over ranks)
+  run_colocated(G, fn) G ranks as threads of one process on one GPU (chase_init_args.colocated)
 """
 from __future__ import annotations
 
@@ -60,3 +61,33 @@ def max_over_ranks(x: float) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def run_colocated(world: int, fn, device: int = 0, timeout: float = 900.0):
+    """Run fn(rank) for rank = 0..world-1 on `world` threads of this process (the co-located mode
+    of chase_init_args.colocated: every rank's handle on `device`, communicators in-process).
+    Returns the per-rank results; re-raises the first rank's exception.  Each rank's collective
+    library calls block until all ranks make them, so the threads must run concurrently (ctypes
+    releases the GIL inside the library)."""
+    import threading
+    results, errors = [None] * world, [None] * world
+
+    def body(rank):
+        try:
+            import torch
+            torch.cuda.set_device(device)
+            results[rank] = fn(rank)
+        except BaseException as e:     # noqa: BLE001 -- re-raised on the caller's thread
+            errors[rank] = e
+
+    threads = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout)
+    if any(t.is_alive() for t in threads):
+        raise TimeoutError(f"co-located ranks did not finish within {timeout} s")
+    for e in errors:
+        if e is not None:
+            raise e
+    return results

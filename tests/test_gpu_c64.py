@@ -93,12 +93,20 @@ def test_c64_emulated_grid_step(lib, grid):
 
 
 def test_c64_rejects_misaligned_shard(lib):
-    ch = lib.Chase(1001, 4, 4, dtype="c64")
-    H = torch.zeros((1001, 1001), dtype=torch.complex64, device="cuda")
-    X = torch.zeros((8, 1001), dtype=torch.complex64, device="cuda").t()
-    Y = torch.zeros((8, 1001), dtype=torch.complex64, device="cuda").t()
-    with pytest.raises(Exception):
+    """TMA layout limits: an odd-order grid is refused at chase_init (the same answer on every
+    rank, decided from N / r / c); an odd ldh or a misaligned H at the call."""
+    from paper_2205_02491_b200._lib import ChaseError
+    with pytest.raises(ChaseError) as e:
+        lib.Chase(1001, 4, 4, dtype="c64")
+    assert e.value.status == 2
+    ch = lib.Chase(1000, 4, 4, dtype="c64")
+    Hp = torch.zeros((1000, 1001), dtype=torch.complex64, device="cuda")
+    H = Hp.t()[:1000, :1000]             # column-major view with ldh = 1001 (odd)
+    X = torch.zeros((8, 1000), dtype=torch.complex64, device="cuda").t()
+    Y = torch.zeros((8, 1000), dtype=torch.complex64, device="cuda").t()
+    with pytest.raises(ChaseError) as e:
         ch.hemm_step(0, H, X, Y, 8, 1.0, 0.0, 0.0)
+    assert e.value.status == 2
 
 
 def test_c64_lanczos_vs_oracle(lib):

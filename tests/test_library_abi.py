@@ -86,3 +86,31 @@ def test_product_package_never_references_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f), errors="replace").read()
                 assert not re.search(r"^\s*(?:import|from)\s+oracle\b|#include\s+[\"<][^\">]*oracle", src, re.M), f
+
+
+def test_init_args_layout_matches_header(tmp_path):
+    """The binding's ctypes chase_init_args / chase_report mirror include/chase.h byte for byte
+    (sizeof and every field offset, from a C program compiled against the header)."""
+    import shutil
+    import subprocess
+    from paper_2205_02491_b200._lib import InitArgs, Report
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    fields = [f for f, _ in InitArgs._fields_]
+    rfields = [f for f, _ in Report._fields_]
+    src = ["#include <stdio.h>", "#include <stddef.h>", '#include "chase.h"', "int main(void) {",
+           '  printf("%zu\\n", sizeof(chase_init_args));']
+    src += [f'  printf("%zu\\n", offsetof(chase_init_args, {f}));' for f in fields]
+    src += ['  printf("%zu\\n", sizeof(chase_report));']
+    src += [f'  printf("%zu\\n", offsetof(chase_report, {f}));' for f in rfields]
+    src += ["  return 0;", "}"]
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    r = subprocess.run(["gcc", "-std=c11", str(c), "-I" + os.path.join(ROOT, "include"), "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(InitArgs)] + [getattr(InitArgs, f).offset for f in fields]
+    want += [ctypes.sizeof(Report)] + [getattr(Report, f).offset for f in rfields]
+    assert got == want
