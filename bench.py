@@ -32,14 +32,29 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N1, NEV, NEX, DEG = 30000, 2250, 750, 20
-FP64_DMMA_PEAK_TFLOPS = 37.12     # measured (profiles/r01_fp64_peak.jsonl), see DESIGN.md
-# The filter GEMM uses the 3M complex product (3 real DMMA per complex multiply-add), so its
-# ceiling in algorithmic complex flops (8 per complex MAC) is 4/3 of the DMMA peak.
-FILTER_PEAK_3M_TFLOPS = FP64_DMMA_PEAK_TFLOPS * 4.0 / 3.0
-# Complex single (tcgen05 kind::tf32, 3xTF32): TF32 dense peak = 1/2 x the measured BF16 peak
-# (MEASURED_PEAKS.json, nominal ratio of the profiling guide); 3 MMAs per real product -> /3.
-BF16_MEASURED_TFLOPS = 1644.0
 METRIC = "filter TFLOP/s, one ChASE subspace iteration (P:727-731), complex double"
+# Roofline denominators measured on a B200 by tools/microbench/peaks.cu (run_peaks.sh): FP64 DMMA
+# (mma.sync.m8n8k4.f64) and tcgen05 kind::tf32, each as a burst (one ~60 ms launch after idle) and
+# sustained (>= 6 s back to back, rate over the last 4 s) figure with the clocks recorded.  The
+# timed regions here are seconds long, so the sustained figures are the denominators.
+PEAKS_FILE = os.path.join(ROOT, "profiles", "r02_peaks.json")
+FALLBACK_DMMA_TFLOPS = 37.12      # r01 short-run measurement (profiles/r01_fp64_peak.jsonl)
+BF16_MEASURED_TFLOPS = 1644.0
+
+
+def load_peaks():
+    """(dmma_tflops, tf32_tflops, source) -- sustained measured figures, else labelled fallbacks."""
+    try:
+        d = json.load(open(PEAKS_FILE))
+        return (d["dmma_f64"]["sustained_tflops"], d["tf32_tcgen05"]["sustained_tflops"],
+                f"{os.path.relpath(PEAKS_FILE, ROOT)} (sustained, measured by tools/microbench/peaks.cu)")
+    except Exception:
+        try:
+            bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", BF16_MEASURED_TFLOPS)
+        except Exception:
+            bf16 = BF16_MEASURED_TFLOPS
+        return (FALLBACK_DMMA_TFLOPS, 0.5 * bf16,
+                "fallback: r01 short-run DMMA figure and 1/2 x measured BF16 (nominal TF32 ratio)")
 
 
 def parse():
@@ -58,6 +73,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c64", action="store_true", help="skip the complex-single filter sub-measurement")
+    ap.add_argument("--no-config3", action="store_true", help="skip the config-3 (N=60000) one-GPU sub-line")
     ap.add_argument("--ref-seconds", type=float, default=None, help=argparse.SUPPRESS)   # tests: bound the oracle sample
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: N = n sqrt(G) (paper P:717-718, default); strong: N = n on every G (config 3)")
@@ -166,6 +182,93 @@ def _cpu_model():
     except OSError:
         pass
     return "unknown"
+
+
+def _threads(n):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n)
+    except Exception:
+        return None
+
+
+def config1_compare(pkg, gpu=True, runs=3):
+    """BASELINE config 1 (N = 1000 complex double Uniform, G1 = Q diag(lambda) Q^H with Haar Q,
+    nev 50, nex 25, deg 20, tol 1e-10): the oracle's full solve, best of `runs`, on 1 host thread
+    and on all host threads, and the GPU solve (best of `runs`), with the
+    eigenvalue agreement of the two."""
+    import numpy as np
+    import oracle
+    from chase_gen import make_matrix
+    N, nev, nex = 1000, 50, 25
+    M = make_matrix("uniform", N, "g1", seed=1)
+    H = M.dense()
+    normH = float(np.max(np.abs(M.lam)))
+    out = {"what": "BASELINE config 1: N=1000 complex double Uniform (G1), nev=50, nex=25, deg=20, tol=1e-10; best of %d" % runs}
+    cores = len(os.sched_getaffinity(0))
+    ovals = None
+    for label, nthr in (("oracle_all_threads_s", cores), ("oracle_1_thread_s", 1)):
+        lim = _threads(nthr)
+        best = float("inf")
+        for _ in range(runs):
+            t0 = time.perf_counter()
+            ovals, _, orep = oracle.chase_solve(H, nev, nex, deg=20, tol=1e-10)
+            best = min(best, time.perf_counter() - t0)
+        if lim is not None:
+            lim.restore_original_limits()
+        out[label] = best
+    out["oracle_threads"] = cores
+    out["oracle_iterations"] = orep.iterations
+    out["oracle_eig_err_rel"] = float(np.max(np.abs(ovals - M.lam[:nev])) / normH)
+    if gpu:
+        import torch
+        dH = torch.from_numpy(np.asfortranarray(H)).t().contiguous().t().cuda()
+        ch = pkg.Chase(N, nev, nex)
+        best, rep = float("inf"), None
+        for _ in range(runs):
+            vals, vecs, rep, st = ch.solve(dH, nev, nex, deg=20, tol=1e-10)
+            best = min(best, rep["t_all"])
+        V = vecs.cpu().numpy()[:, :nev]
+        out.update(gpu_s=best, gpu_iterations=rep["iterations"], gpu_status=st,
+                   gpu_eig_err_rel=float(np.max(np.abs(vals - M.lam[:nev])) / normH),
+                   gpu_vs_oracle_eig_rel=float(np.max(np.abs(vals - ovals)) / normH),
+                   gpu_resid_rel=float(np.max(np.linalg.norm(H @ V - V * vals[None, :], axis=0)) / normH),
+                   speedup_vs_oracle_all_threads=out["oracle_all_threads_s"] / best)
+        ch.close()
+    return out
+
+
+def projected_oracle_tts(rate_tflops, cases):
+    """projected oracle time-to-solution for the large configs = (measured
+    matvecs x 8 N^2 + iterations x the per-iteration QR / RR terms) / the oracle's measured rate.
+    Per-iteration terms with n = nev + nex (an upper bound: locking shrinks n): RR's H Q 8 N^2 n,
+    plus 40 N n^2 for Householder QR + its Q (16 N n^2), Q^H (HQ) (8), Q Z (8) and (HQ) Z (8)."""
+    out = []
+    for c in cases:
+        N, n = float(c["N"]), float(c["nev"] + c["nex"])
+        flops = 8.0 * N * N * c["matvecs"] + c["iterations"] * (8.0 * N * N * n + 40.0 * N * n * n)
+        out.append(dict(c, projected_oracle_s=flops / (rate_tflops * 1e12), label="projected"))
+    return out
+
+
+def _recorded_tts():
+    """Measured (matvecs, iterations) of the large configs from committed GPU runs (profiles/)."""
+    cases = []
+    for f, cfg in (("r01_config4_121_4gpu_tts.json", "config4 1-2-1"),
+                   ("r01_config4_wilkinson_4gpu_tts.json", "config4 Wilkinson")):
+        try:
+            lines = [ln for ln in open(os.path.join(ROOT, "profiles", f)) if ln.startswith("{")]
+            d = json.loads(lines[-1])
+            t = d.get("time_to_solution", d)
+            cases.append({"config": cfg, "N": d.get("N", d.get("config", {}).get("N")),
+                          "nev": d.get("nev", d.get("config", {}).get("nev")),
+                          "nex": d.get("nex", d.get("config", {}).get("nex")),
+                          "matvecs": t["matvecs"], "iterations": t["iterations"],
+                          "gpu_s": t.get("t_all_s", t.get("s")), "gpus": d.get("gpus", d.get("n_gpus")),
+                          "source": "profiles/" + f})
+        except Exception:
+            continue
+    return cases
 
 
 def run_reference(args, out):
@@ -283,7 +386,9 @@ def main():
     phases = {k: max_over_ranks(sum(r[k] for r in reps)) / args.steps
               for k in ("t_lanczos", "t_filter", "t_qr", "t_rr", "t_resid", "t_all")}
 
-    # ---- end-to-end through the C ABI with host buffers (H2D of H + D2H of the eigenpairs)
+    # ---- end-to-end through the C ABI with HOST buffers: chase_solve reads the shard from pinned
+    #      host memory and writes the eigenvectors to host memory; the copies run inside the call,
+    #      every step, and the whole call is timed (wall clock around a synchronous call)
     e2e = None
     if not args.no_e2e:
         try:
@@ -295,28 +400,22 @@ def main():
             vh = torch.empty((nev, q), dtype=torch.complex128).t()
             pinned = False
         Hh.copy_(H)
-        Hd = torch.empty_like(H)
-        e2e_steps = max(1, min(args.steps, 2))
+        ch.solve(Hh, nev, nex, deg=DEG, tol=1e-10, vectors=vh)          # warm-up (staging buffer)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
         mv = 0
-        for _ in range(e2e_steps):
-            Hd.copy_(Hh, non_blocking=True)
-            vals, _, rep, st = ch.solve(Hd, nev, nex, deg=DEG, tol=1e-10, vectors=vecs)
-            vh.copy_(vecs[:, :nev], non_blocking=True)
+        for _ in range(args.steps):
+            vals, _, rep, st = ch.solve(Hh, nev, nex, deg=DEG, tol=1e-10, vectors=vh)
             mv += rep["matvecs"]
-        ev1.record()
-        torch.cuda.synchronize()
-        e2e_s = max_over_ranks(max(ev0.elapsed_time(ev1) * 1e-3, time.perf_counter() - t0))
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": 8.0 * N * N * mv / e2e_s / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": 16 * p * q, "d2h_bytes_per_step": 16 * q * nev + 8 * nev,
-               "steps": e2e_steps, "pinned_host": pinned}
-        del Hh, Hd, vh
+               "steps": args.steps, "pinned_host": pinned,
+               "how": "chase_solve(H_shard in host memory, ritz_vectors in host memory): the C-ABI call copies "
+                      "the shard H2D and the eigenvectors D2H itself; wall time of the synchronous calls, max over ranks"}
+        del Hh, vh
 
     # ---- roofline of the dominant kernel (filter GEMM): algorithmic FLOPs / measured filter time
     per_launch_flops = 8.0 * p * q * (nev + nex)        # first iteration: every column at every degree step
@@ -332,12 +431,9 @@ def main():
     # ---- complex-single filter on the same workload shape: H rounded to
     #      complex64 once (untimed), chase_filter with every column at degree 20 (20 fused steps)
     c64 = None
+    dmma_peak, tf32_peak, peak_src = load_peaks()
     if world == 1 and not args.no_c64:
-        try:
-            bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", BF16_MEASURED_TFLOPS)
-        except Exception:
-            bf16 = BF16_MEASURED_TFLOPS
-        peak64 = bf16 * 0.5 / 3.0
+        peak64 = tf32_peak / 3.0
         H32 = H.to(torch.complex64)
         ch32 = pkg.Chase(N, nev, nex, dtype="c64", device=local, stream=stream)
         V32 = (vecs[:, :nev + nex]).to(torch.complex64)
@@ -360,7 +456,7 @@ def main():
         c64 = {"what": "chase_filter in complex single (CHASE_C64: tcgen05 kind::tf32 3xTF32 on CTA pairs), "
                        f"N={N}, {nev + nex} columns at degree {DEG}, same Uniform H rounded to complex64",
                "tflops": a64, "peak": peak64, "frac": a64 / peak64, "unit": "TFLOP/s", "s_per_filter": t64 / reps64,
-               "peak_source": f"1/2 x measured BF16 {bf16} TFLOP/s (TF32 nominal ratio) / 3 MMAs per real product"}
+               "peak_source": f"TF32 tcgen05 peak {tf32_peak:.1f} TFLOP/s ({peak_src}) / 3 MMAs per real product (3xTF32)"}
         ch32.close()
         del H32, V32, W32
         torch.cuda.empty_cache()
@@ -375,6 +471,36 @@ def main():
                "matvecs": rep["matvecs"], "filter_tflops_per_gpu": 8.0 * N * N * rep["matvecs"] / world / max(rep["t_filter"], 1e-12) / 1e12,
                "max_abs_eig_err_rel": float(np.max(np.abs(vals - lam)) / np.max(np.abs(M.lam)))}
     ch.close()
+    del H, vecs
+    torch.cuda.empty_cache()
+
+    # ---- BASELINE config 3 on one GPU (N = 60000 Geometric, nev 1000, nex 300; the largest
+    #      single-GPU BASELINE config): one subspace iteration, 1 warm-up + 1 timed
+    cfg3 = None
+    if world == 1 and not args.no_config3 and (args.n, nev, nex) == (N1, NEV, NEX):
+        N3, nev3, nex3 = 60000, 1000, 300
+        M3 = G2Matrix(spectrum("geometric", N3), seed=1)
+        H3 = torch.empty((N3, N3), dtype=torch.complex128, device="cuda").t()
+        DeviceG2(M3).fill(H3, 0, 0)
+        torch.cuda.synchronize()
+        ch3 = pkg.Chase(N3, nev3, nex3, device=local, stream=stream)
+        ch3.set_option("max_iter", 1)
+        v3 = torch.empty((nev3 + nex3, N3), dtype=torch.complex128, device="cuda").t()
+        ch3.solve(H3, nev3, nex3, deg=DEG, tol=1e-10, vectors=v3)
+        _, _, r3, _ = ch3.solve(H3, nev3, nex3, deg=DEG, tol=1e-10, vectors=v3)
+        f3 = 8.0 * N3 * N3 * r3["matvecs"]
+        cfg3 = {"workload": f"config3: N={N3} complex double geometric, nev={nev3}, nex={nex3}, deg={DEG}, one subspace "
+                            "iteration (P:727-731), 1x1; 1 warm-up + 1 timed iteration",
+                "value": f3 / r3["t_all"] / 1e12, "unit": "TFLOP/s", "ms_per_step": r3["t_all"] * 1e3,
+                "filter_tflops": f3 / r3["t_filter"] / 1e12,
+                "roofline_frac": f3 / r3["t_filter"] / 1e12 / (dmma_peak * 4.0 / 3.0),
+                "phases_s": {k: r3[k] for k in ("t_lanczos", "t_filter", "t_qr", "t_rr", "t_resid", "t_all")}}
+        ch3.close()
+        del H3, v3
+        torch.cuda.empty_cache()
+    cfg1 = None
+    if world == 1 and not args.no_cpu:
+        cfg1 = config1_compare(pkg)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -390,20 +516,33 @@ def main():
                 "wall_ms_per_step": t_wall / args.steps * 1e3,
                 "phases_s_per_step": phases,
                 "filter_tflops_per_gpu": achieved,
-                "roofline": {"bound": "tensor", "achieved": achieved, "peak": FILTER_PEAK_3M_TFLOPS, "unit": "TFLOP/s",
-                             "frac": achieved / FILTER_PEAK_3M_TFLOPS, "traffic": traffic,
+                "roofline": {"bound": "tensor", "achieved": achieved, "peak": dmma_peak * 4.0 / 3.0, "unit": "TFLOP/s",
+                             "frac": achieved / (dmma_peak * 4.0 / 3.0), "traffic": traffic,
                              "kernel": "zgemm3m_dmma_kernel (filter step: 3M complex product on FP64 DMMA.8x8x4, TMA-staged)",
                              "per_launch_flops": per_launch_flops, "launches": launches_filter,
-                             "dmma_pipe_frac": achieved * 0.75 / FP64_DMMA_PEAK_TFLOPS,
-                             "peak_source": "4/3 x the measured FP64 DMMA.8x8x4 peak 37.12 TFLOP/s (profiles/r01_fp64_peak.jsonl; all 148 SMs at 1965 MHz): 3M spends 3 real DMMA MACs per complex MAC; MEASURED_PEAKS.json has no FP64 entry"},
+                             "dmma_pipe_frac": achieved * 0.75 / dmma_peak,
+                             "peak_source": f"4/3 x the FP64 DMMA.8x8x4 peak {dmma_peak:.2f} TFLOP/s ({peak_src}): 3M spends 3 real DMMA MACs per complex MAC; MEASURED_PEAKS.json has no FP64 entry"},
                 "clocks": clocks, "gpu_launches": launches, "e2e": e2e}
         if tts:
             line["time_to_solution"] = tts
         if c64:
             line["c64_filter"] = c64
+        if cfg3:
+            line["config3_1gpu"] = cfg3
         if world == 1 and not args.no_cpu:
             v, cores, sample = oracle_sample(N, seconds=12.0, family=args.family)
-            line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample}
+            lim = _threads(1)
+            v1, _, _ = oracle_sample(N, seconds=6.0, family=args.family)
+            if lim is not None:
+                lim.restore_original_limits()
+            cases = _recorded_tts()
+            if tts:
+                cases.insert(0, {"config": "config2", "N": N, "nev": nev, "nex": nex, "matvecs": tts["matvecs"],
+                                 "iterations": tts["iterations"], "gpu_s": tts["s"], "gpus": 1,
+                                 "source": "this run's time_to_solution"})
+            line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
+                                    "value_1_thread": v1, "config1_full_solve": cfg1,
+                                    "projected_time_to_solution": projected_oracle_tts(v, cases)}
         print(json.dumps(line), file=out, flush=True)
     if world > 1:
         dist.barrier()

@@ -128,9 +128,11 @@ chase_status chase_set_option(chase_handle* h, const char* key, double value);
 chase_status chase_local_layout(const chase_handle* h, int64_t* row0, int64_t* p, int64_t* col0,
                                 int64_t* q);
 
-/* Alg. 1.  H_shard: device, p x q, ldh >= p, read-only.  ritz_values: host, nev
- * doubles, ascending.  ritz_vectors: device, V-layout q x (nev) with leading dim ldv >= q (if
- * approx=1 it must hold >= nev+nex columns with the initial V-hat on entry).  report may be NULL.
+/* Alg. 1.  H_shard: p x q, ldh >= p, read-only; device memory, or host memory
+ * (pinned or pageable), in which case this call copies it into a library-owned device buffer
+ * (one shard-sized allocation, kept for later calls).  ritz_values: host, nev doubles, ascending.
+ * ritz_vectors: V-layout q x (nev) with leading dim ldv >= q, device or host memory (if approx=1
+ * it must hold >= nev+nex columns with the initial V-hat on entry).  report may be NULL.
  * Returns CHASE_E_MAXITER with the locked pairs valid if max_iter is reached. */
 chase_status chase_solve(chase_handle* h, const void* H_shard, int64_t ldh, int64_t N, int32_t nev,
                          int32_t nex, int32_t deg, double tol, double* ritz_values,

@@ -253,7 +253,7 @@ const void* c64_shadow(chase_handle* h, const void* H, int64_t ldh) {
 
 // H_lo for the shard (recomputed when the caller's H pointer or ld changes)
 void c64_check_call(chase_handle* h, const void* H, int64_t ldh, int ncols) {
-  if (ldh % 2 != 0 || (reinterpret_cast<uintptr_t>(H) % 16) != 0)
+  if (H && (ldh % 2 != 0 || (reinterpret_cast<uintptr_t>(H) % 16) != 0))
     throw UsageError("CHASE_C64 needs an even ldh and a 16-byte aligned H shard");
   if (ncols > h->n_e_max) throw UsageError("c64: ncols exceeds nev_max + nex_max");
 }

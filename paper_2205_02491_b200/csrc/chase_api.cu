@@ -382,6 +382,16 @@ const char* chase_version(void) {
 
 const char* chase_last_error(const chase_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
+// true for host memory (pinned or pageable), false for device / managed memory
+static bool host_ptr(const void* ptr) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+}
+
 // Auto grid (ledger #19): r x c = world, r <= c, |r - c| minimal.
 static void auto_grid(int ws, int& r, int& c) {
   r = 1;
@@ -647,7 +657,7 @@ chase_status chase_solve(chase_handle* h, const void* H, int64_t ldh, int64_t N,
     if (nev + nex > h->n_e_max) throw UsageError("nev + nex exceeds nev_max + nex_max of chase_init");
     if (!H || ldh < h->grid.rows.len || !ritz_values || !ritz_vectors || ldv < h->grid.cols.len)
       throw UsageError("bad pointers / leading dimensions");
-    if (h->c64()) c64_check_call(h, H, ldh, nev + nex);
+    if (h->c64()) c64_check_call(h, host_ptr(H) ? nullptr : H, host_ptr(H) ? 0 : ldh, nev + nex);
     if (h->dtype == CHASE_C128 && h->opt.mixed_filter > 0.0) {
       if (!c64_grid_layout_ok(h->grid))
         throw UsageError("mixed_filter needs every shard of the grid to have q % 4 == 0 and even p");
@@ -655,7 +665,38 @@ chase_status chase_solve(chase_handle* h, const void* H, int64_t ldh, int64_t N,
     return CHASE_OK;
   }, [&]() {
     order_after_user(h);
-    return solve(h, H, ldh, nev, nex, deg, tol, ritz_values, ritz_vectors, ldv, report);
+    // Host buffers (pinned or pageable) are accepted for the shard and the vectors: the shard is
+    // copied into a library-owned device buffer (ld p) and the vectors staged through one, inside
+    // this call -- the end-to-end path of a caller whose H lives in host memory.
+    const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
+    const size_t es = h->es();
+    const void* Hd = H;
+    int64_t ldhd = ldh;
+    if (host_ptr(H)) {
+      h->Hstage.alloc(es * (size_t)p * q);
+      CHASE_CUDA(cudaMemcpy2DAsync(h->Hstage.p, es * p, H, es * ldh, es * p, q, cudaMemcpyHostToDevice, h->stream));
+      Hd = h->Hstage.p;
+      ldhd = p;
+      h->hlo_src = nullptr;            // derived copies of the shard are keyed by pointer: rebuild
+      h->h32_src = nullptr;
+    }
+    void* Vd = ritz_vectors;
+    int64_t ldvd = ldv;
+    const bool vhost = host_ptr(ritz_vectors);
+    if (vhost) {
+      h->Vstage.alloc(es * (size_t)q * (nev + nex));
+      Vd = h->Vstage.p;
+      ldvd = q;
+      if (h->opt.approx)
+        CHASE_CUDA(cudaMemcpy2DAsync(Vd, es * q, ritz_vectors, es * ldv, es * q, nev + nex, cudaMemcpyHostToDevice,
+                                     h->stream));
+    }
+    const chase_status st = solve(h, Hd, ldhd, nev, nex, deg, tol, ritz_values, Vd, ldvd, report);
+    if (vhost) {
+      CHASE_CUDA(cudaMemcpy2DAsync(ritz_vectors, es * ldv, Vd, es * q, es * q, nev, cudaMemcpyDeviceToHost, h->stream));
+      sync_stream(h, h->stream);
+    }
+    return st;
   });
 }
 
@@ -677,7 +718,7 @@ chase_status chase_finalize(chase_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   chase::peer_release(h);
   for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo,
-                         &h->c64v, &h->c64w, &h->H32})
+                         &h->c64v, &h->c64w, &h->H32, &h->Hstage, &h->Vstage})
     b->release();
   heev_work_release(h->jacobi);
   h->jacobi = nullptr;

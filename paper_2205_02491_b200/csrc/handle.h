@@ -102,6 +102,7 @@ struct chase_handle {
   chase::DBuf Hlo;                     // c64: 3xTF32 lo part of the caller's H shard
   chase::DBuf c64v, c64w;              // c64: planar V-layout / W-layout operand formats (c64.cu)
   chase::DBuf H32;                     // f4: complex-single shadow of a complex-double shard
+  chase::DBuf Hstage, Vstage;          // chase_solve with host buffers: device copies of H / vectors
   const void* h32_src = nullptr;
   int64_t h32_ld = 0;
   const void* hlo_src = nullptr;
