@@ -12,6 +12,7 @@
 #include <vector>
 #include "cgemm_tc.cuh"
 #include "handle.h"
+#include "trace.h"
 
 namespace chase {
 
@@ -423,6 +424,8 @@ static int64_t c64_filter_t(chase_handle* h, const void* H, int64_t ldh, TV* V, 
       sigma_prev = sigma;
     }
     const int nk = ncols - first;
+    nvtx_push_step(k, (k & 1) ? 0 : 1, nk);
+    struct PopAtEnd { ~PopAtEnd() { nvtx_pop(); } } pop_at_end;
     VFmt v = vfmt(h, ncap, first);
     WFmt w = wfmt(h, ncap, first);
     const int cn = (k & 1) ? g.c : g.r;

@@ -8,6 +8,7 @@
 #include "handle.h"
 #include "linalg.h"
 #include "rng.cuh"
+#include "trace.h"
 
 using namespace chase;
 
@@ -155,6 +156,8 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       sigma_prev = sigma;
     }
     const int dir = (k & 1) ? 0 : 1;        // odd: forward V -> W; even: backward W -> V
+    nvtx_push_step(k, dir, ncols - first);
+    struct PopAtEnd { ~PopAtEnd() { nvtx_pop(); } } pop_at_end;
     char* X = dir == 0 ? Vz : Wz;
     char* Y = dir == 0 ? Wz : Vz;
     const int64_t ldx = dir == 0 ? ldv : ldw, ldy = dir == 0 ? ldw : ldv;
@@ -524,7 +527,8 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     if (!key) throw UsageError("null option key");
     std::string k(key);
     if (k == "deg_max") { if (v < 2) throw UsageError("deg_max >= 2"); h->opt.deg_max = (int)v; }
-    else if (k == "max_iter") { if (v < 1) throw UsageError("max_iter >= 1"); h->opt.max_iter = (int)v; }
+    else if (k == "max_iter") { if (v < 0) throw UsageError("max_iter >= 0 (0 = auto)"); h->opt.max_iter = (int)v; }
+    else if (k == "stall_iter") { if (v < 1) throw UsageError("stall_iter >= 1"); h->opt.stall_iter = (int)v; }
     else if (k == "lanczos_steps") { if (v < 2) throw UsageError("lanczos_steps >= 2"); h->opt.lanczos_steps = (int)v; }
     else if (k == "lanczos_runs") { if (v < 1) throw UsageError("lanczos_runs >= 1"); h->opt.lanczos_runs = (int)v; }
     else if (k == "seed_v") h->opt.seed_v = (uint64_t)v;

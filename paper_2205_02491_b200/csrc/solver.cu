@@ -25,6 +25,7 @@
 #include "handle.h"
 #include "linalg.h"
 #include "scalar.cuh"
+#include "trace.h"
 
 namespace chase {
 
@@ -141,9 +142,11 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
   t_all.start(st);
 
   // ---- Alg. 1 line 2: Lanczos bounds
+  nvtxRangePushA("Lanczos");
   t_lz.start(st);
   LanczosOut lz = lanczos(h, Hv, ldh, n_e);
   t_lz.stop(st);
+  nvtxRangePop();
   double b_sup = lz.b_sup, mu_1 = lz.mu_1, mu_ne = lz.mu_ne;
   const double nu = lz.nu > 0.0 ? lz.nu : 1.0;
 
@@ -177,7 +180,16 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
   int64_t matvecs = 0;
   double max_resid = 0.0;
 
-  while (locked < nev && it < h->opt.max_iter) {                // line 3
+  // max_iter = 0 (default, ledger #21 reading revised): iterate while the solve makes progress --
+  // a new locked pair, or the smallest active residual below 0.9 x its best so far -- and stop
+  // with CHASE_E_MAXITER after stall_iter iterations without progress or kAutoIterCap in total.
+  // (The 1-2-1 family at N = 115000 needs 103 iterations, past a fixed cap of 100.)
+  constexpr int kAutoIterCap = 5000;
+  const bool auto_iter = h->opt.max_iter <= 0;
+  const int max_it = auto_iter ? kAutoIterCap : h->opt.max_iter;
+  int last_progress = 0;
+  double best_res = 1e300;
+  while (locked < nev && it < max_it) {                          // line 3
     ++it;
     const int n_act = n_e - locked;
     T* Va = V + (int64_t)locked * q;
@@ -185,6 +197,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     T* HVa = HV + (int64_t)locked * p;
 
     // ---- line 4: Filter
+    nvtxRangePushA("Filter");
     t_f.start(st);
     const bool f4_now = f4 && f4_next;
     if constexpr (SC<T>::is_complex) {
@@ -198,8 +211,10 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
       matvecs += filter(h, Hv, ldh, Va, q, Wa, p, n_act, m.data() + locked, b_sup, mu_1, mu_ne);
     }
     t_f.stop(st);
+    nvtxRangePop();
 
     // ---- line 5: QR([Y V]) -- CGS2 against the locked Y, then CholQR2 (shifted fallback)
+    nvtxRangePushA("QR");
     t_qr.start(st);
     for (int pass = 0; pass < 2 && locked > 0; ++pass) {
       ZgemmDesc d;                                  // T = Y^H Va   (locked x n_act)
@@ -253,8 +268,10 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
       copy2d<T>(Va, q, V2, q, q, n_act, st);
     }
     t_qr.stop(st);
+    nvtxRangePop();
 
     // ---- line 6: Rayleigh-Ritz
+    nvtxRangePushA("RR");
     t_rr.start(st);
     if constexpr (SC<T>::is_complex) {
       if (mixed)
@@ -293,8 +310,10 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
       gemm(h, e);
     }
     t_rr.stop(st);
+    nvtxRangePop();
 
     // ---- line 7: residuals  ||H v - theta v|| over I_ij, summed over the world
+    nvtxRangePushA("Resid");
     t_res.start(st);
     if (I.len > 0)
       resid_norms2<T>(Wa + (I.start - r0), p, Va + (I.start - c0), q, d_theta, I.len, n_act, d_res2, part, st);
@@ -302,6 +321,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
       CHASE_CUDA(cudaMemsetAsync(d_res2, 0, sizeof(double) * n_act, st));
     allreduce_doubles(h, h->world, d_res2, n_act);
     t_res.stop(st);
+    nvtxRangePop();
     CHASE_CUDA(cudaMemcpyAsync(th_h.data(), d_theta, sizeof(double) * n_act, cudaMemcpyDeviceToHost, st));
     CHASE_CUDA(cudaMemcpyAsync(r2_h.data(), d_res2, sizeof(double) * n_act, cudaMemcpyDeviceToHost, st));
     sync_stream(h, st);
@@ -324,6 +344,13 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     int nl = 0;
     while (nl < n_act && res[locked + nl] <= tol) ++nl;
     locked += nl;
+    {
+      double rmin = 1e300;
+      for (int a = locked; a < n_e; ++a) rmin = std::min(rmin, res[a]);
+      if (nl > 0 || rmin < 0.9 * best_res) last_progress = it;
+      best_res = std::min(best_res, rmin);
+    }
+    if (auto_iter && locked < nev && it - last_progress >= h->opt.stall_iter) break;
     // ---- line 9-10: bounds and interval
     mu_1 = *std::min_element(ritz.begin(), ritz.end());
     mu_ne = *std::max_element(ritz.begin(), ritz.end());
@@ -399,7 +426,10 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     rep->max_resid = max_resid;
   }
   if (locked < nev) {
-    h->err = "max_iter reached with " + std::to_string(locked) + " of " + std::to_string(nev) + " pairs locked";
+    const std::string why = auto_iter && it < max_it
+                                ? "no progress in stall_iter iterations: stopped after " + std::to_string(it) + " iterations with "
+                                : std::string("max_iter reached with ");
+    h->err = why + std::to_string(locked) + " of " + std::to_string(nev) + " pairs locked";
     return CHASE_E_MAXITER;
   }
   return CHASE_OK;
