@@ -68,11 +68,18 @@ static ZgemmDesc step_desc(chase_handle* h, int dir, const void* H, int64_t ldh,
   return d;
 }
 
+// local product of a step: FP64 DMMA GEMM, or (f4, fp64_emulation > 0, complex double) the
+// Ozaki-scheme emulation on the INT8 tensor cores (ozaki.cu)
+static void step_gemm(chase_handle* h, const ZgemmDesc& d) {
+  if (h->dtype == CHASE_C128 && h->opt.fp64_emulation > 0 && !d.red) ozaki_step(h, d);
+  else gemm(h, d);
+}
+
 void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
                void* Y, int64_t ldy, int ncols, double alpha, double beta, double gamma) {
   if (ncols <= 0) return;
   const Grid& g = h->grid;
-  gemm(h, step_desc(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma));
+  step_gemm(h, step_desc(h, dir, H, ldh, X, ldx, Y, ldy, ncols, alpha, beta, gamma));
   if (dir == 0)
     allreduce_block(h, h->rowc, Y, g.rows.len, ldy, ncols);     // row communicator
   else
@@ -134,7 +141,7 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
   const int max_tiles = h->real() ? std::max(dgemm_tiles((int)pmax, ncols), dgemm_tiles((int)qmax, ncols))
                                   : std::max(zgemm3m_tiles((int)pmax, ncols), zgemm3m_tiles((int)qmax, ncols));
   const bool fused = comm && ldv == g.cols.len && ldw == g.rows.len && inside(h->V, V) && inside(h->W, W) &&
-                     peer_tiles_fit(max_tiles) && peer_reduce_ready(h);
+                     h->opt.fp64_emulation == 0 && peer_tiles_fit(max_tiles) && peer_reduce_ready(h);
   if (fused) {
     nchunks = 1;
     peer_enter(h);                // every rank has entered this filter call (peer-timeout skew guard)
@@ -185,8 +192,8 @@ int64_t filter(chase_handle* h, const void* H, int64_t ldh, void* V, int64_t ldv
       const int lo = std::max(first, bnd[ch]), hi = bnd[ch + 1];
       if (lo >= hi) continue;
       if (rec[(k - 1) & 1][ch]) CHASE_CUDA(cudaStreamWaitEvent(h->stream, h->ev_comm[(k - 1) & 1][ch], 0));
-      gemm(h, step_desc(h, dir, H, ldh, X + (int64_t)lo * ldx * es, ldx, Y + (int64_t)lo * ldy * es, ldy, hi - lo,
-                        alpha, beta, c));
+      step_gemm(h, step_desc(h, dir, H, ldh, X + (int64_t)lo * ldx * es, ldx, Y + (int64_t)lo * ldy * es, ldy,
+                             hi - lo, alpha, beta, c));
       CHASE_CUDA(cudaEventRecord(h->ev_gemm[ch], h->stream));
       CHASE_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_gemm[ch], 0));
       cudaStream_t saved = h->stream;
@@ -540,6 +547,10 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     else if (k == "fused_reduce") h->opt.fused_reduce = v != 0.0;
     else if (k == "fused_reduce_c64") h->opt.fused_reduce_c64 = v != 0.0;
     else if (k == "peer_timeout") { if (!(v > 0)) throw UsageError("peer_timeout > 0"); h->opt.peer_timeout = v; }
+    else if (k == "fp64_emulation") {
+      if (v != 0 && (v < 3 || v > 8)) throw UsageError("fp64_emulation: 0 (off) or 3..8 slices");
+      h->opt.fp64_emulation = (int)v;
+    }
     else if (k == "comm_timeout") { if (v < 0) throw UsageError("comm_timeout >= 0"); h->opt.comm_timeout = v; }
     else throw UsageError("unknown option " + k);
     return CHASE_OK;
@@ -721,6 +732,7 @@ chase_status chase_finalize(chase_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   chase::peer_release(h);
+  chase::ozaki_release(h);
   for (chase::DBuf* b : {&h->V, &h->W, &h->HV, &h->V2, &h->G, &h->G2, &h->Z, &h->scratch, &h->red, &h->lz, &h->Hlo,
                          &h->c64v, &h->c64w, &h->H32, &h->Hstage, &h->Vstage})
     b->release();

@@ -79,6 +79,7 @@ struct Options {
   bool fused_reduce_c64 = false;  // f1 for the complex-single filter (measured slower than NCCL + rebuild)
   double peer_timeout = 120.0;    // f1: seconds a rank waits for its peers' tiles before failing
   double comm_timeout = 0.0;      // host waits poll ncclCommGetAsyncError; > 0: also fail after this many s
+  int fp64_emulation = 0;         // f4: > 0 = complex-double filter products on INT8 tensor cores (Ozaki, S slices)
 };
 
 }  // namespace chase
@@ -104,6 +105,13 @@ struct chase_handle {
   chase::DBuf c64v, c64w;              // c64: planar V-layout / W-layout operand formats (c64.cu)
   chase::DBuf H32;                     // f4: complex-single shadow of a complex-double shard
   chase::DBuf Hstage, Vstage;          // chase_solve with host buffers: device copies of H / vectors
+  struct OzShard {                     // fp64_emulation: int8 slices of the shard per direction (ozaki.cu)
+    const void* src = nullptr;
+    int64_t ld = 0;
+    int S = 0;
+    chase::DBuf slices, exps, diag;
+  } oz_fwd, oz_bwd;
+  chase::DBuf oz_b, oz_t;              // fp64_emulation: slices of the block X, FP64 product accumulators
   const void* h32_src = nullptr;
   int64_t h32_ld = 0;
   const void* hlo_src = nullptr;
@@ -182,6 +190,9 @@ const PeerRed* peer_red_for(chase_handle* h, int dir, const void* Y);
 void peer_wait(chase_handle* h, int tiles);
 void peer_check(chase_handle* h);
 void peer_release(chase_handle* h);
+// f4 (ozaki.cu): one local fused step with the complex products emulated on INT8 tensor cores
+void ozaki_step(chase_handle* h, const ZgemmDesc& d);
+void ozaki_release(chase_handle* h);
 // tile count of one fused step fits the arrival counters (else the step all-reduces with NCCL)
 bool peer_tiles_fit(int tiles);
 // barrier over the world before a fused filter (ranks enter within the peer timeout of each other)

@@ -1,0 +1,639 @@
+// f4 research branch: the complex-double filter step with its
+// FP64 products emulated on the INT8 tensor cores (tcgen05.mma kind::i8) by the Ozaki scheme
+// (error-free splitting into int8 slices, exact int32 products, FP64 recombination).
+//
+// Arithmetic.  A complex product C = A B runs as Gauss's 3M on real matrices, T1 = Ar Br,
+// T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi); Re C = T1 - T2, Im C = T3 - T1 - T2 (as in zgemm3m.cuh).
+// Each real product P = X Y is emulated: every row m of X is scaled by 2^-e_m (e_m = frexp
+// exponent of the row's max |x|, so |x| 2^-e_m < 1) and cut into S truncated 7-bit slices,
+//   x 2^-e_m = sum_{s=1..S} a_s 2^-7s + r,   a_s in [-127, 127] (int8),  |r| < 2^-7S,
+// every column n of Y likewise (exponent f_n, slices b_t).  Then
+//   P_mn = 2^(e_m + f_n) sum_{s+t <= S+1} 2^-7(s+t) (A_s B_t)_mn  + O(S 2^-7S) |X||Y| (normwise),
+// the (A_s B_t) are exact int32 tensor-core products, and terms of equal d = s + t share one
+// int32 accumulator (up to floor((2^31 - 1) / (127^2 K)) products per accumulator, so the sum is
+// exact).  With S = 7 the truncation error is ~2^-49 |X||Y| per entry, below the FP64 step bar
+// of 1e-13 by two orders of magnitude.
+//
+// Data.  The H shard's slices are built once per shard (and direction): forward A = H (rows of H
+// contiguous in k: a transposing slicer), backward A = H^H (columns of H contiguous in k; the
+// imaginary part negated).  Every step slices the block X (columns contiguous in k).  All slice
+// matrices are K-major int8 [slice][row][ldk], TMA-loaded as 128-byte swizzled rows.
+//
+// Kernel (oz_gemm_kernel): persistent CTA pairs (tcgen05 cta_group::2), 256 x 256 output tiles,
+// 192 threads per CTA: warp 0 TMA producer into a 6-stage ring (16 KB of A rows + 16 KB of B
+// columns per CTA and stage), one elected lane of the leader's warp 1 issues 4
+// tcgen05.mma.kind::i8 (M = 256, N = 256, K = 32) per stage into one of two 256-column int32
+// TMEM accumulators (all slice pairs of the launch accumulate into it), warps 2-5 drain it
+// (tcgen05.ld 32x32b) and add 2^-7d x acc into the FP64 accumulator of the real product while
+// the next tile accumulates.  Tiles are rastered N-fastest, so concurrently running pairs share
+// each A panel (the large H slices) through L2.
+// The final oz_combine kernel forms the 3M combination with the exponent scalings and the fused
+// step epilogue  Y = alpha (C - gamma E X) + beta Y.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <type_traits>
+#include <vector>
+#include "dense.h"
+#include "handle.h"
+#include "tma.cuh"
+
+namespace chase {
+
+namespace oz {
+constexpr int BM = 128, BN = 256, BK = 128;            // per CTA: 128 rows; per pair: 256 x 256; BK int8 (= bytes)
+constexpr uint32_t A_BYTES = BM * BK, B_BYTES = (BN / 2) * BK, STAGE_BYTES = A_BYTES + B_BYTES;   // 16 + 16 KB
+constexpr int STAGES = 6;
+constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+constexpr int THREADS = 192;
+constexpr int MAX_PAIRS = 8;
+constexpr uint32_t TCOLS = 2 * BN;                      // two 256-column int32 accumulators (double buffer)
+
+struct Params {
+  int M, N, K;
+  int npairs;
+  int sa[MAX_PAIRS], tb[MAX_PAIRS];    // slice index of A and of B for every pair of the launch
+  double scale;                        // 2^-7d
+  double* out;                         // FP64 accumulator of the real product (M x N, ld ldo)
+  int64_t ldo;
+  int accumulate;                      // 0: out = scale acc; 1: out += scale acc
+};
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {   // K-major, SWIZZLE_128B, 8-row groups 1 KB apart
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa0(uint32_t addr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(0));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_3d_pair(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAITOZ:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONEOZ;\n"
+      "bra LAB_WAITOZ;\n"
+      "DONEOZ:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void commit_both(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+
+// Persistent CTA-pair kernel (cluster of 2, tcgen05 cta_group::2): every pair walks the 256 x 256
+// output tiles t = pair, pair + npair, ... (N fastest, so concurrently running pairs share A
+// panels in L2).  Per tile and k block of 128, each CTA stages its 128 A rows and its half (128
+// columns) of B for every slice pair of the launch; the leader's MMA warp issues 4
+// tcgen05.mma.cta_group::2.kind::i8 (M = 256, N = 256, K = 32) per stage into one of two
+// 256-column TMEM accumulators, so the drain of tile t overlaps the MMAs of tile t + 1.  Drain:
+// 4 warps per CTA (TMEM lane quadrant = warp % 4), 16 columns at a time, 2^-7d x acc added
+// into the FP64 output.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, Params p) {
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + 2 * BM - 1) / (2 * BM);
+  const int T = tiles_n * tiles_m;
+  const int pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
+  const int KT = (p.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tA);
+      tma_prefetch_desc(&tB);
+      int it = 0;
+      for (int t = pair; t < T; t += npair) {
+        const int m0 = (t / tiles_n) * 2 * BM + (int)rank * BM;
+        const int nh = (t % tiles_n) * BN + (int)rank * (BN / 2);
+        for (int kt = 0; kt < KT; ++kt) {
+          for (int q = 0; q < p.npairs; ++q, ++it) {
+            const int s = it % STAGES;
+            if (it >= STAGES) mbar_wait(empty + s, ((it / STAGES) - 1) & 1);
+            const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+            const uint32_t fb = mapa0(smem_u32(full + s));
+            if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * STAGE_BYTES);
+            tma_3d_pair(st, &tA, kt * BK, m0, p.sa[q], fb);
+            tma_3d_pair(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      uint32_t leader;
+      asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+      // S32 accumulate, signed int8 A and B, both K-major, N = 256, M = 256 (pair)
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)((2 * BM) >> 4) << 24);
+      int it = 0, tl = 0;
+      for (int t = pair; t < T; t += npair, ++tl) {
+        const int b = tl & 1;
+        if (tl >= 2) {
+          wait_cluster(acc_empty + b, ((tl >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        const uint32_t td = tm + (uint32_t)b * BN;
+        for (int j = 0; j < KT * p.npairs; ++j, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full + s, (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (leader) {
+            const uint32_t sa = smem_u32(sm + s * STAGE_BYTES), sb = sa + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 32; ++kk) {
+              const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+              asm volatile(
+                  "{ .reg .pred q; setp.ne.b32 q, %4, 0; tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, q; }"
+                  ::"r"(td), "l"(sdesc(sa + kk * 32)), "l"(sdesc(sb + kk * 32)), "r"(idesc), "r"(acc));
+            }
+            commit_both(empty + s);
+          }
+          __syncwarp();
+        }
+        if (leader) commit_both(acc_full + b);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
+    int tl = 0;
+    for (int t = pair; t < T; t += npair, ++tl) {
+      const int b = tl & 1;
+      const int row = (t / tiles_n) * 2 * BM + (int)rank * BM + 32 * quad + lane;
+      const int n0 = (t % tiles_n) * BN;
+      mbar_wait(acc_full + b, (tl >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t base = tm + lane_off + (uint32_t)b * BN;
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(base + c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (row < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = n0 + c0 + j;
+            if (n < p.N) {
+              double* o = p.out + (int64_t)row + (int64_t)n * p.ldo;
+              const double v = p.scale * (double)(int)r[j];
+              *o = p.accumulate ? *o + v : v;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bar = mapa0(smem_u32(acc_empty + b));
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(TCOLS));
+}
+
+// ------------------------------------------------------------------------------- slicing
+// exponent e with 128 max 2^-e < 127.5 (so the first round-to-nearest slice stays in int8),
+// 0 for an all-zero line
+__device__ __forceinline__ int line_exp(double mx) {
+  int e = 0;
+  if (mx > 0.0) {
+    frexp(mx, &e);
+    if (ldexp(mx, 7 - e) >= 127.5) ++e;
+  }
+  return e;
+}
+
+// S round-to-nearest 7-bit slices of v (|v| 128 < 127.5): a_s = rint(r 2^7), r <- r 2^7 - a_s
+// (exact in FP64).  |a_1| <= 127, |a_s| <= 64 after that; the remainder is <= 2^-7S / 2 and,
+// unlike truncation, unbiased (measured: ~7x smaller product error than truncated slices).
+template <int S>
+__device__ __forceinline__ void cut(double v, int8_t (&a)[S]) {
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    v *= 128.0;
+    const double t = rint(v);
+    a[s] = (int8_t)(int)t;
+    v -= t;
+  }
+}
+
+// Lines contiguous in memory (columns of a column-major complex matrix): line c of `rows`
+// complex values at X + c ld.  Writes, for P in {re, im (negated if conj), re + im}, slices
+// out[(P S + s) * plane + c * ldk + k] and exponents e[P * lines + c].  One CTA per line.
+// diag != INT_MIN: the element k = c + diag of line c lies on the global diagonal of H; it is left
+// out of the slices (zero) and added exactly in FP64 by oz_combine (diagonal split: the dominant
+// diagonal of a Hermitian H would otherwise set the line's exponent and cost the off-diagonal
+// entries their low bits).
+template <int S>
+__global__ void __launch_bounds__(256) oz_slice_lines(const double2* X, int64_t ld, int rows, int lines, int conj,
+                                                      int diag, int8_t* out, int64_t ldk, int64_t plane, int* e) {
+  const int c = blockIdx.x;
+  const double2* x = X + (int64_t)c * ld;
+  const double sg = conj ? -1.0 : 1.0;
+  const int kd = diag == INT_MIN ? -1 : c + diag;
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  for (int k = threadIdx.x; k < rows; k += 256) {
+    if (k == kd) continue;
+    const double2 v = x[k];
+    m0 = fmax(m0, fabs(v.x));
+    m1 = fmax(m1, fabs(v.y));
+    m2 = fmax(m2, fabs(v.x + sg * v.y));
+  }
+  __shared__ double sm[3][8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+    m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sm[0][threadIdx.x >> 5] = m0;
+    sm[1][threadIdx.x >> 5] = m1;
+    sm[2][threadIdx.x >> 5] = m2;
+  }
+  __syncthreads();
+  __shared__ int ex[3];
+  if (threadIdx.x < 3) {
+    double m = 0.0;
+    for (int w = 0; w < 8; ++w) m = fmax(m, sm[threadIdx.x][w]);
+    ex[threadIdx.x] = line_exp(m);
+    e[threadIdx.x * lines + c] = ex[threadIdx.x];
+  }
+  __syncthreads();
+  const double sc0 = ldexp(1.0, -ex[0]), sc1 = ldexp(1.0, -ex[1]), sc2 = ldexp(1.0, -ex[2]);
+  for (int k = threadIdx.x; k < (int)ldk; k += 256) {
+    int8_t a0[S], a1[S], a2[S];
+    if (k < rows && k != kd) {
+      const double2 v = x[k];
+      const double im = sg * v.y;
+      cut<S>(v.x * sc0, a0);
+      cut<S>(im * sc1, a1);
+      cut<S>((v.x + im) * sc2, a2);
+    } else {
+#pragma unroll
+      for (int s = 0; s < S; ++s) a0[s] = a1[s] = a2[s] = 0;
+    }
+    int8_t* o = out + (int64_t)c * ldk + k;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      o[(int64_t)(0 * S + s) * plane] = a0[s];
+      o[(int64_t)(1 * S + s) * plane] = a1[s];
+      o[(int64_t)(2 * S + s) * plane] = a2[s];
+    }
+  }
+}
+
+// Row maxima of a column-major complex matrix (rows of H for the forward A operand): |re|,
+// |im|, |re + im| per row, as order-preserving bit patterns (non-negative doubles) via atomicMax.
+__global__ void oz_row_max(const double2* H, int64_t ld, int rows, int cols, int diag, unsigned long long* mx) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= rows) return;
+  const int c0 = blockIdx.y * 256, c1 = min(cols, c0 + 256);
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  for (int j = c0; j < c1; ++j) {
+    if (j == i + diag) continue;                      // diagonal split (see oz_slice_lines)
+    const double2 v = H[i + (int64_t)j * ld];
+    m0 = fmax(m0, fabs(v.x));
+    m1 = fmax(m1, fabs(v.y));
+    m2 = fmax(m2, fabs(v.x + v.y));
+  }
+  atomicMax(mx + i, (unsigned long long)__double_as_longlong(m0));
+  atomicMax(mx + rows + i, (unsigned long long)__double_as_longlong(m1));
+  atomicMax(mx + 2 * rows + i, (unsigned long long)__double_as_longlong(m2));
+}
+
+// Transposing slicer for the forward A operand: row i of H (strided) -> line i of the output
+// (contiguous in k = column index j).  Tile of 32 rows x 64 columns through shared memory.
+template <int S>
+__global__ void __launch_bounds__(256) oz_slice_rows(const double2* H, int64_t ld, int rows, int cols, int diag,
+                                                     const unsigned long long* mx, int8_t* out, int64_t ldk,
+                                                     int64_t plane, int* e) {
+  __shared__ double2 t[64][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 64;
+  for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
+    const int ii = idx & 31, jj = idx >> 5;
+    const int i = i0 + ii, j = j0 + jj;
+    t[jj][ii] = (i < rows && j < cols && j != i + diag) ? H[i + (int64_t)j * ld] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  // thread -> (row ii, 8-column group): 8 consecutive k per slice
+  const int ii = threadIdx.x >> 3, jg = (threadIdx.x & 7) * 8;
+  const int i = i0 + ii;
+  if (i >= rows) return;
+  int ex[3];
+#pragma unroll
+  for (int P = 0; P < 3; ++P) ex[P] = line_exp(__longlong_as_double((long long)mx[P * rows + i]));
+  if (blockIdx.y == 0 && (threadIdx.x & 7) == 0) {
+#pragma unroll
+    for (int P = 0; P < 3; ++P) e[P * rows + i] = ex[P];
+  }
+  const double sc0 = ldexp(1.0, -ex[0]), sc1 = ldexp(1.0, -ex[1]), sc2 = ldexp(1.0, -ex[2]);
+#pragma unroll 1
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = j0 + jg + jj;
+    if (j >= (int)ldk) break;
+    const double2 v = t[jg + jj][ii];
+    int8_t a0[S], a1[S], a2[S];
+    cut<S>(v.x * sc0, a0);
+    cut<S>(v.y * sc1, a1);
+    cut<S>((v.x + v.y) * sc2, a2);
+    int8_t* o = out + (int64_t)i * ldk + j;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      o[(int64_t)(0 * S + s) * plane] = a0[s];
+      o[(int64_t)(1 * S + s) * plane] = a1[s];
+      o[(int64_t)(2 * S + s) * plane] = a2[s];
+    }
+  }
+}
+
+// Y = alpha (C - gamma E X) + beta Y from the three FP64 real products (3M) with their exponents
+// rows m in [dlo, dhi) carry the diagonal split and the shift: + alpha (hdiag[m] - gamma) X[m + doff]
+__global__ void oz_combine(const double* T, int64_t ldt, int64_t tplane, const int* eA, int M, const int* fB, int N,
+                           double2* Y, int64_t ldy, double alpha, double beta, int beta_on, const double2* X,
+                           int64_t ldx, const double2* hdiag, int dlo, int dhi, int64_t doff, double gamma) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(idx % M), n = (int)(idx / M);
+    const int64_t o = (int64_t)m + (int64_t)n * ldt;
+    const double t1 = ldexp(T[o], eA[m] + fB[n]);
+    const double t2 = ldexp(T[tplane + o], eA[M + m] + fB[N + n]);
+    const double t3 = ldexp(T[2 * tplane + o], eA[2 * M + m] + fB[2 * N + n]);
+    double re = alpha * (t1 - t2), im = alpha * (t3 - t1 - t2);
+    if (m >= dlo && m < dhi) {
+      const double2 x = X[(int64_t)m + doff + (int64_t)n * ldx];
+      const double2 hd = hdiag[m];
+      const double dr = hd.x - gamma;
+      re += alpha * (dr * x.x - hd.y * x.y);
+      im += alpha * (dr * x.y + hd.y * x.x);
+    }
+    double2* y = Y + (int64_t)m + (int64_t)n * ldy;
+    if (beta_on) {
+      const double2 yo = *y;
+      re += beta * yo.x;
+      im += beta * yo.y;
+    }
+    *y = make_double2(re, im);
+  }
+}
+
+// the diagonal element of output row m (forward: H[m][m + off]; backward: conj(H[m - off][m])),
+// zero where row m does not cross the global diagonal (off = r0 - c0)
+__global__ void oz_diag(const double2* H, int64_t ld, int p, int q, int dir, int off, double2* d) {
+  const int m = blockIdx.x * 256 + threadIdx.x;
+  const int lines = dir == 0 ? p : q;
+  if (m >= lines) return;
+  double2 v = make_double2(0.0, 0.0);
+  if (dir == 0) {
+    const int j = m + off;
+    if (j >= 0 && j < q) v = H[m + (int64_t)j * ld];
+  } else {
+    const int i = m - off;
+    if (i >= 0 && i < p) { v = H[i + (int64_t)m * ld]; v.y = -v.y; }
+  }
+  d[m] = v;
+}
+
+// 3-D int8 tensor map over [slice][line][ldk] (dims {K, lines, slices}), box {128, box_lines, 1}
+void make_slice_tmap(CUtensorMap* map, const int8_t* base, int64_t K, int64_t lines, int64_t ldk, int slices,
+                     int box_lines) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CHASE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)lines, (cuuint64_t)slices};
+  cuuint64_t strides[2] = {(cuuint64_t)ldk, (cuuint64_t)(ldk * lines)};
+  cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)box_lines, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (ozaki slices) failed: " + std::to_string((int)r));
+}
+
+inline int64_t ldk_of(int64_t K) { return (K + 127) / 128 * 128; }   // 16-B TMA strides, whole k tiles
+}  // namespace oz
+
+// ------------------------------------------------------------------------------------ host
+using OzShard = chase_handle::OzShard;    // slices of the shard for one direction (cached on the handle)
+
+static int oz_slices_opt(chase_handle* h) { return std::min(8, std::max(0, h->opt.fp64_emulation)); }
+
+template <int S>
+static void slice_lines(const double2* X, int64_t ld, int rows, int lines, bool conj, int diag, int8_t* out,
+                        int64_t ldk, int64_t plane, int* e, cudaStream_t st) {
+  if (lines <= 0) return;
+  oz::oz_slice_lines<S><<<lines, 256, 0, st>>>(X, ld, rows, lines, conj ? 1 : 0, diag, out, ldk, plane, e);
+  CHASE_CHECK_LAUNCH();
+}
+
+template <int S>
+static void slice_rows(const double2* H, int64_t ld, int rows, int cols, int diag, unsigned long long* mx,
+                       int8_t* out, int64_t ldk, int64_t plane, int* e, cudaStream_t st) {
+  CHASE_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * 3 * rows, st));
+  oz::oz_row_max<<<dim3(ceil_div(rows, 256), ceil_div(cols, 256)), 256, 0, st>>>(H, ld, rows, cols, diag, mx);
+  CHASE_CHECK_LAUNCH();
+  oz::oz_slice_rows<S><<<dim3(ceil_div(rows, 32), ceil_div(ldk, 64)), 256, 0, st>>>(H, ld, rows, cols, diag, mx, out,
+                                                                                    ldk, plane, e);
+  CHASE_CHECK_LAUNCH();
+}
+
+template <class F>
+static void with_S(int S, F&& f) {
+  switch (S) {
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 5: f(std::integral_constant<int, 5>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    case 7: f(std::integral_constant<int, 7>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    default: throw UsageError("fp64_emulation: slices must be 3..8");
+  }
+}
+
+// the A operand of direction dir for this shard: slices [3 S][lines][ldk] + exponents [3][lines]
+static const OzShard& oz_shard(chase_handle* h, int dir, const void* H, int64_t ldh) {
+  OzShard& z = dir == 0 ? h->oz_fwd : h->oz_bwd;
+  const int S = oz_slices_opt(h);
+  if (z.src == H && z.ld == ldh && z.S == S && z.slices.p) return z;
+  const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
+  const int lines = dir == 0 ? (int)p : (int)q, K = dir == 0 ? (int)q : (int)p;
+  const int64_t ldk = oz::ldk_of(K);
+  z.slices.alloc((size_t)3 * S * lines * ldk);
+  z.exps.alloc(sizeof(int) * 3 * (size_t)lines + sizeof(unsigned long long) * 3 * (size_t)lines + 16);
+  int* e = z.exps.as<int>();
+  unsigned long long* mx = reinterpret_cast<unsigned long long*>(e + 3 * (size_t)lines + (3 * lines & 1));
+  const double2* Hz = reinterpret_cast<const double2*>(H);
+  // diagonal split: global diagonal of H in local coordinates (row i, column i + (r0 - c0))
+  const int64_t r0 = h->grid.rows.start, c0 = h->grid.cols.start;
+  with_S(S, [&](auto Sc) {
+    constexpr int SS = decltype(Sc)::value;
+    if (dir == 0)
+      slice_rows<SS>(Hz, ldh, (int)p, (int)q, (int)(r0 - c0), mx, z.slices.as<int8_t>(), ldk, (int64_t)lines * ldk, e,
+                     h->stream);
+    else   // A = H^H: line j = column j of H, conjugated; its diagonal element is row j + (c0 - r0)
+      slice_lines<SS>(Hz, ldh, (int)p, (int)q, true, (int)(c0 - r0), z.slices.as<int8_t>(), ldk, (int64_t)lines * ldk,
+                      e, h->stream);
+  });
+  z.diag.alloc(sizeof(double2) * (size_t)lines);
+  oz::oz_diag<<<ceil_div(lines, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, dir, (int)(r0 - c0),
+                                                          z.diag.as<double2>());
+  CHASE_CHECK_LAUNCH();
+  z.src = H;
+  z.ld = ldh;
+  z.S = S;
+  return z;
+}
+
+// Y = alpha (op(H) X - gamma E X) + beta Y  (one rank's local part of a fused step, complex double)
+void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
+  const int S = oz_slices_opt(h);
+  const int dir = d.conjA ? 1 : 0;
+  const OzShard& A = oz_shard(h, dir, d.A, d.lda);
+  const int M = d.M, N = d.N, K = d.K;
+  if (M <= 0 || N <= 0) return;
+  cudaStream_t st = h->stream;
+  // B operand: the block X (columns contiguous in k)
+  const int64_t ldkb = oz::ldk_of(K);
+  h->oz_b.alloc((size_t)3 * S * N * ldkb + sizeof(int) * 3 * (size_t)N + 64);
+  int8_t* bsl = h->oz_b.as<int8_t>();
+  int* fB = reinterpret_cast<int*>(bsl + (size_t)3 * S * N * ldkb);
+  with_S(S, [&](auto Sc) {
+    slice_lines<decltype(Sc)::value>(reinterpret_cast<const double2*>(d.B), d.ldb, K, N, false, INT_MIN, bsl, ldkb,
+                                     (int64_t)N * ldkb, fB, st);
+  });
+  // FP64 accumulators of the three real products
+  h->oz_t.alloc(sizeof(double) * 3 * (size_t)M * N);
+  double* T = h->oz_t.as<double>();
+  static unsigned long long attr = 0;
+  if (first_on_device(attr))
+    CHASE_CUDA(cudaFuncSetAttribute(oz::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
+  const int lines_a = M;
+  const int64_t ldka = oz::ldk_of(K);
+  // pairs per int32 accumulator: npairs 127^2 K <= 2^31 - 1 (exact accumulation)
+  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(oz::MAX_PAIRS, 2147483647LL / (16129LL * K)));
+  if (16129LL * K > 2147483647LL) throw UsageError("fp64_emulation: K > 133143 needs K chunking (not built)");
+  const int ptiles = ceil_div(M, 2 * oz::BM) * ceil_div(N, oz::BN);
+  int sms = 148;
+  {
+    int dev = 0;
+    CHASE_CUDA(cudaGetDevice(&dev));
+    CHASE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int grid = 2 * std::min(ptiles, sms / 2);            // persistent: one CTA pair per 2 SMs
+  for (int P = 0; P < 3; ++P) {
+    CUtensorMap ta, tb;
+    oz::make_slice_tmap(&ta, A.slices.as<int8_t>() + (size_t)P * S * lines_a * ldka, K, lines_a, ldka, S, oz::BM);
+    oz::make_slice_tmap(&tb, bsl + (size_t)P * S * N * ldkb, K, N, ldkb, S, oz::BN / 2);
+    bool first = true;
+    for (int dsum = 2; dsum <= S + 1; ++dsum) {
+      std::vector<std::pair<int, int>> pairs;
+      for (int s = 1; s < dsum; ++s)
+        if (s <= S && dsum - s <= S) pairs.push_back({s - 1, dsum - s - 1});
+      for (size_t b0 = 0; b0 < pairs.size(); b0 += cap) {
+        oz::Params prm{};
+        prm.M = M; prm.N = N; prm.K = K;
+        prm.npairs = (int)std::min<size_t>(cap, pairs.size() - b0);
+        for (int q = 0; q < prm.npairs; ++q) {
+          prm.sa[q] = pairs[b0 + q].first;
+          prm.tb[q] = pairs[b0 + q].second;
+        }
+        prm.scale = std::ldexp(1.0, -7 * dsum);
+        prm.out = T + (size_t)P * M * N;
+        prm.ldo = M;
+        prm.accumulate = first ? 0 : 1;
+        first = false;
+        oz::oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(ta, tb, prm);
+        CHASE_CHECK_LAUNCH();
+      }
+    }
+  }
+  const int* eA = A.exps.as<int>();
+  // intersection rows of this direction (the diagonal split and the shift live there)
+  const Grid& g = h->grid;
+  const int64_t r0 = g.rows.start, c0 = g.cols.start, p = g.rows.len, q = g.cols.len;
+  int dlo, dhi;
+  int64_t doff;
+  if (dir == 0) {
+    dlo = (int)std::max<int64_t>(0, c0 - r0); dhi = (int)std::min<int64_t>(p, c0 + q - r0); doff = r0 - c0;
+  } else {
+    dlo = (int)std::max<int64_t>(0, r0 - c0); dhi = (int)std::min<int64_t>(q, r0 + p - c0); doff = c0 - r0;
+  }
+  oz::oz_combine<<<148 * 8, 256, 0, st>>>(T, M, (int64_t)M * N, eA, M, fB, N, reinterpret_cast<double2*>(d.C), d.ldc,
+                                          d.alpha, d.beta, d.beta != 0.0 ? 1 : 0,
+                                          reinterpret_cast<const double2*>(d.B), d.ldb, A.diag.as<double2>(), dlo,
+                                          std::max(dlo, dhi), doff, d.gamma);
+  CHASE_CHECK_LAUNCH();
+}
+
+void ozaki_release(chase_handle* h) {
+  for (OzShard* z : {&h->oz_fwd, &h->oz_bwd}) {
+    z->slices.release();
+    z->exps.release();
+    z->diag.release();
+    z->src = nullptr;
+  }
+  h->oz_b.release();
+  h->oz_t.release();
+}
+
+}  // namespace chase

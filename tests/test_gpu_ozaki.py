@@ -1,0 +1,98 @@
+"""f4 research branch: complex-double filter steps with the FP64 products emulated on the INT8
+tensor cores (Ozaki scheme; csrc/ozaki.cu, option fp64_emulation = S slices).
+
+  * exactness: operands that are small integers times powers of two are represented exactly by
+    the first slices, so the emulated product must equal the exact product bit for bit (the int8
+    tcgen05 MMA, the TMA operand layout, the slice recombination and the 3M combination are all
+    checked by this one identity);
+  * accuracy: one fused step (shift, beta, both directions, ragged M / N / K) vs oracle.hemm_step
+    at the complex-double bar 1e-13 for S = 7; the error falls with S as
+    ~2^-7S (table in DESIGN.md);
+  * the filter and a whole solve with emulated products meet the complex-double bars."""
+import numpy as np
+import pytest
+
+import oracle
+from chase_gen import make_matrix
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _dev(a):
+    return torch.from_numpy(np.asfortranarray(a)).t().contiguous().t().cuda()
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("direction", [0, 1])
+@pytest.mark.parametrize("N,n", [(600, 37), (777, 300), (130, 1)])
+def test_emulated_product_is_exact_on_representable_inputs(direction, N, n):
+    import paper_2205_02491_b200 as pkg
+    rng = np.random.default_rng(N + n)
+    Hr, Hi = rng.integers(-100, 101, (N, N)), rng.integers(-100, 101, (N, N))
+    Xr, Xi = rng.integers(-50, 51, (N, n)), rng.integers(-50, 51, (N, n))
+    H = (Hr + 1j * Hi) * 2.0 ** -10          # not Hermitian: the step does not need it
+    X = (Xr + 1j * Xi) * 2.0 ** -3
+    # exact integer products (int64), scaled by 2^-13 (exact in FP64: |sums| < 2^53)
+    if direction == 0:
+        Ar, Ai = Hr, Hi
+    else:                                   # op(H) = H^H
+        Ar, Ai = Hr.T, -Hi.T
+    re = Ar @ Xr - Ai @ Xi
+    im = Ar @ Xi + Ai @ Xr
+    ref = (re + 1j * im) * 2.0 ** -13
+    ch = pkg.Chase(N, n, 1)
+    ch.set_option("fp64_emulation", 7)
+    dY = _dev(np.zeros((N, n), dtype=complex))
+    ch.hemm_step(direction, _dev(H), _dev(X), dY, n, 1.0, 0.0, 0.0)
+    assert np.array_equal(dY.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("direction", [0, 1])
+@pytest.mark.parametrize("N,n", [(1000, 75), (1300, 257), (333, 7)])
+def test_emulated_step_vs_oracle(direction, N, n):
+    import paper_2205_02491_b200 as pkg
+    M = make_matrix("uniform", N, "g2", seed=N)
+    H = M.dense()
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
+    Y0 = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
+    ref = oracle.hemm_step(H, X, Y0, 0.37, -0.81, 0.55)
+    ch = pkg.Chase(N, n, 1)
+    ch.set_option("fp64_emulation", 7)
+    dY = _dev(Y0)
+    ch.hemm_step(direction, _dev(H), _dev(X), dY, n, 0.37, -0.81, 0.55)
+    err = _rel(dY.cpu().numpy(), ref)
+    assert err <= 1e-13, err
+    # beta = 0 must not read Y (NaN poison)
+    dY = torch.full((n, N), complex(np.nan, np.nan), dtype=torch.complex128).cuda().t()
+    ch.hemm_step(direction, _dev(H), _dev(X), dY, n, 1.0, 0.0, 0.0)
+    assert _rel(dY.cpu().numpy(), H @ X) <= 1e-13
+
+
+def test_emulated_filter_and_solve():
+    import paper_2205_02491_b200 as pkg
+    N, nev, nex = 900, 40, 20
+    M = make_matrix("wilkinson", N, "g2", seed=7)
+    H = M.dense()
+    degrees = np.sort(np.array([0, 2, 4, 6, 10, 20, 36] + [20] * 30))
+    V = oracle.random_block(5, 0, N, 0, len(degrees), 0)
+    b_sup, mu_1, mu_ne = M.lam[-1] * 1.01, M.lam[0], M.lam[60]
+    fref, mv = oracle.chebyshev_filter(H, V, degrees, b_sup, mu_1, mu_ne)
+    ch = pkg.Chase(N, nev, nex)
+    ch.set_option("fp64_emulation", 7)
+    dH, dV = _dev(H), _dev(V)
+    dW = _dev(np.zeros((N, len(degrees)), dtype=complex))
+    assert ch.filter(dH, dV, dW, degrees, b_sup, mu_1, mu_ne) == mv
+    out = dV.cpu().numpy()
+    colerr = np.linalg.norm(out - fref, axis=0) / np.linalg.norm(fref, axis=0)
+    assert np.max(colerr) <= 1e-11
+    vals, vecs, rep, st = ch.solve(dH, nev, nex, deg=20, tol=1e-10)
+    assert st == 0
+    normH = np.max(np.abs(M.lam))
+    assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
+    Vv = vecs.cpu().numpy()[:, :nev]
+    assert np.max(np.linalg.norm(H @ Vv - Vv * vals[None, :], axis=0)) <= 1e-10 * normH

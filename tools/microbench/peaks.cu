@@ -49,7 +49,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
 constexpr int TM = 128, TN = 256;
 constexpr int GROUP = 32;                    // MMAs per commit group
 
-__global__ void __launch_bounds__(128, 1) tf32_loop(int groups, float* out) {
+// KIND 0: kind::tf32 (F32 accumulate); KIND 1: kind::i8 (signed int8 A/B, S32 accumulate).  Both
+// read 32-byte K slices of the 128-byte swizzled rows (8 tf32 or 32 int8 per MMA).
+template <int KIND>
+__global__ void __launch_bounds__(128, 1) mma_loop(int groups, float* out) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = sm;                    // 128 rows x 128 B (32 tf32 of k), K-major, SW128
@@ -57,7 +60,8 @@ __global__ void __launch_bounds__(128, 1) tf32_loop(int groups, float* out) {
   __shared__ uint64_t bar[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32;
-  // random operands (a hash of the byte offset): realistic toggling in the datapath
+  // random operands (a hash of the byte offset): realistic toggling in the datapath (for i8 the
+  // same words read as four int8 values each)
   uint32_t* w = reinterpret_cast<uint32_t*>(sm);
   for (int i = threadIdx.x; i < (TM + TN) * 32; i += blockDim.x) {
     uint32_t x = (uint32_t)i * 2654435761u + blockIdx.x * 40503u;
@@ -81,8 +85,10 @@ __global__ void __launch_bounds__(128, 1) tf32_loop(int groups, float* out) {
     uint32_t leader;
     asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
     if (leader) {
-      // F32 accumulate, TF32 A and B, both K-major, N = 256, M = 128
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+      // tf32: F32 accumulate (1 << 4), TF32 A / B (2 << 7, 2 << 10); i8: S32 accumulate (2 << 4),
+      // signed 8-bit A / B (1 << 7, 1 << 10); both K-major, N = 256, M = 128
+      const uint32_t idesc = (KIND == 0 ? ((1u << 4) | (2u << 7) | (2u << 10)) : ((2u << 4) | (1u << 7) | (1u << 10))) |
+                             ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
       uint32_t phase[2] = {0, 0};
       for (int g = 0; g < groups; ++g) {
         const int b = g & 1;
@@ -97,8 +103,12 @@ __global__ void __launch_bounds__(128, 1) tf32_loop(int groups, float* out) {
           const uint64_t da = sdesc(su32(sA) + kk * 32, 16, 1024);
           const uint64_t db = sdesc(su32(sB) + kk * 32, 16, 1024);
           const uint32_t acc = (g > 0 || i > 0) ? 1u : 0u;
-          asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
-                       ::"r"(tmem_base), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          if constexpr (KIND == 0)
+            asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
+                         ::"r"(tmem_base), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          else
+            asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
+                         ::"r"(tmem_base), "l"(da), "l"(db), "r"(idesc), "r"(acc));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar[b])));
       }
@@ -180,10 +190,18 @@ int main() {
   // TF32 tcgen05: one CTA per SM, 2 x 128 x 256 x 8 flop per MMA
   {
     const int smem = (TM + TN) * 128 + 1024;
-    CK(cudaFuncSetAttribute(tf32_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(mma_loop<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int groups = 30000;
     const double flop = 2.0 * TM * TN * 8.0 * GROUP * groups * sms;
-    if (measure("tcgen05_mma_kind_tf32_m128n256k8", flop, [&] { tf32_loop<<<sms, 128, smem>>>(groups, d); }, 60)) return 1;
+    if (measure("tcgen05_mma_kind_tf32_m128n256k8", flop, [&] { mma_loop<0><<<sms, 128, smem>>>(groups, d); }, 60)) return 1;
+  }
+  // INT8 tcgen05 (the Ozaki-scheme FP64 emulation's engine): 2 x 128 x 256 x 32 ops per MMA
+  {
+    const int smem = (TM + TN) * 128 + 1024;
+    CK(cudaFuncSetAttribute(mma_loop<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int groups = 60000;
+    const double ops = 2.0 * TM * TN * 32.0 * GROUP * groups * sms;
+    if (measure("tcgen05_mma_kind_i8_m128n256k32", ops, [&] { mma_loop<1><<<sms, 128, smem>>>(groups, d); }, 60)) return 1;
   }
   return 0;
 }
