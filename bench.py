@@ -43,18 +43,19 @@ BF16_MEASURED_TFLOPS = 1644.0
 
 
 def load_peaks():
-    """(dmma_tflops, tf32_tflops, source) -- sustained measured figures, else labelled fallbacks."""
+    """(dmma_tflops, tf32_tflops, int8_tops, source) -- sustained measured figures, else labelled fallbacks."""
     try:
         d = json.load(open(PEAKS_FILE))
         return (d["dmma_f64"]["sustained_tflops"], d["tf32_tcgen05"]["sustained_tflops"],
+                d["i8_tcgen05"]["sustained_tflops"],
                 f"{os.path.relpath(PEAKS_FILE, ROOT)} (sustained, measured by tools/microbench/peaks.cu)")
     except Exception:
         try:
             bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", BF16_MEASURED_TFLOPS)
         except Exception:
             bf16 = BF16_MEASURED_TFLOPS
-        return (FALLBACK_DMMA_TFLOPS, 0.5 * bf16,
-                "fallback: r01 short-run DMMA figure and 1/2 x measured BF16 (nominal TF32 ratio)")
+        return (FALLBACK_DMMA_TFLOPS, 0.5 * bf16, 2.0 * bf16,
+                "fallback: r01 short-run DMMA figure; 1/2 and 2 x measured BF16 (nominal TF32 / INT8 ratios)")
 
 
 def parse():
@@ -74,6 +75,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c64", action="store_true", help="skip the complex-single filter sub-measurement")
     ap.add_argument("--no-config3", action="store_true", help="skip the config-3 (N=60000) one-GPU sub-line")
+    ap.add_argument("--fp64", default="ozaki", choices=["ozaki", "dmma"],
+                    help="complex-double products: ozaki = FP64 emulated on the INT8 tensor cores (library "
+                         "default, fp64_emulation = 7), dmma = FP64 DMMA")
     ap.add_argument("--ref-seconds", type=float, default=None, help=argparse.SUPPRESS)   # tests: bound the oracle sample
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: N = n sqrt(G) (paper P:717-718, default); strong: N = n on every G (config 3)")
@@ -350,6 +354,8 @@ def main():
                    stream=stream)
     assert ch.local_layout() == (row0, p, col0, q)
     ch.set_option("max_iter", 1)
+    EMU = 7 if args.fp64 == "ozaki" else 0
+    ch.set_option("fp64_emulation", EMU)
     vecs = torch.empty((nev + nex, q), dtype=torch.complex128, device="cuda").t()
 
     def step():
@@ -417,21 +423,53 @@ def main():
                       "the shard H2D and the eigenvectors D2H itself; wall time of the synchronous calls, max over ranks"}
         del Hh, vh
 
-    # ---- roofline of the dominant kernel (filter GEMM): algorithmic FLOPs / measured filter time
+    # ---- roofline of the dominant kernel: algorithmic FLOPs / measured filter time
     per_launch_flops = 8.0 * p * q * (nev + nex)        # first iteration: every column at every degree step
     launches_filter = DEG * args.steps
     achieved = flops / world / filt_s_max / 1e12
+    dmma_peak, tf32_peak, i8_peak, peak_src = load_peaks()
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_filter_gemm.json")
+    prof = os.path.join(ROOT, "profiles", "r02_ncu_ozaki_step.json" if EMU else "r01_ncu_filter_gemm.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("dram_bytes_per_step" if EMU else "dram_bytes_per_launch")
         except Exception:
             traffic = None
+    if EMU:
+        # a complex MAC costs 3 real products (3M) x S(S+1)/2 slice products = 84 int8 MACs (168 ops)
+        # for 8 algorithmic flop: the emulation's ceiling is the INT8 tensor peak x 8 / 168
+        pairs = EMU * (EMU + 1) // 2
+        peak_c = i8_peak * 8.0 / (2.0 * 3 * pairs)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_c, "unit": "TFLOP/s", "frac": achieved / peak_c,
+                "traffic": traffic,
+                "kernel": "oz_gemm_kernel (filter step: FP64 complex product emulated on INT8 tcgen05 MMAs, Ozaki "
+                          f"scheme, {EMU} slices, 3M; + slicing / recombination kernels, all inside the timed filter phase)",
+                "per_launch_flops": per_launch_flops, "launches": launches_filter, "unit_of_launch": "one fused filter step",
+                "int8_pipe_frac": achieved / peak_c,
+                "peak_source": f"INT8 tcgen05 peak {i8_peak:.0f} TOPS ({peak_src}) x 8 / {2 * 3 * pairs} "
+                               "(int8 ops per algorithmic complex flop)"}
+    else:
+        roof = {"bound": "tensor", "achieved": achieved, "peak": dmma_peak * 4.0 / 3.0, "unit": "TFLOP/s",
+                "frac": achieved / (dmma_peak * 4.0 / 3.0), "traffic": traffic,
+                "kernel": "zgemm3m_dmma_kernel (filter step: 3M complex product on FP64 DMMA.8x8x4, TMA-staged)",
+                "per_launch_flops": per_launch_flops, "launches": launches_filter,
+                "dmma_pipe_frac": achieved * 0.75 / dmma_peak,
+                "peak_source": f"4/3 x the FP64 DMMA.8x8x4 peak {dmma_peak:.2f} TFLOP/s ({peak_src}): 3M spends 3 real "
+                               "DMMA MACs per complex MAC; MEASURED_PEAKS.json has no FP64 entry"}
+    # ---- the other complex-double product path on the same H, one iteration (context)
+    other = None
+    if world == 1 and not args.no_c64:
+        ch.set_option("fp64_emulation", 0 if EMU else 7)
+        _, _, ro, _ = ch.solve(H, nev, nex, deg=DEG, tol=1e-10, vectors=vecs)
+        ch.set_option("fp64_emulation", EMU)
+        fo = 8.0 * N * N * ro["matvecs"]
+        other = {"what": ("FP64 DMMA" if EMU else "Ozaki INT8 emulation (fp64_emulation = 7)")
+                 + " complex-double products, one iteration on the same H (context for the main line)",
+                 "value": fo / ro["t_all"] / 1e12, "filter_tflops": fo / ro["t_filter"] / 1e12,
+                 "ms_per_step": ro["t_all"] * 1e3, "unit": "TFLOP/s"}
     # ---- complex-single filter on the same workload shape: H rounded to
     #      complex64 once (untimed), chase_filter with every column at degree 20 (20 fused steps)
     c64 = None
-    dmma_peak, tf32_peak, peak_src = load_peaks()
     if world == 1 and not args.no_c64:
         peak64 = tf32_peak / 3.0
         H32 = H.to(torch.complex64)
@@ -485,12 +523,13 @@ def main():
         torch.cuda.synchronize()
         ch3 = pkg.Chase(N3, nev3, nex3, device=local, stream=stream)
         ch3.set_option("max_iter", 1)
+        ch3.set_option("fp64_emulation", 0)     # the Ozaki slices of a 57.6 GB shard (151 GB) do not fit beside it
         v3 = torch.empty((nev3 + nex3, N3), dtype=torch.complex128, device="cuda").t()
         ch3.solve(H3, nev3, nex3, deg=DEG, tol=1e-10, vectors=v3)
         _, _, r3, _ = ch3.solve(H3, nev3, nex3, deg=DEG, tol=1e-10, vectors=v3)
         f3 = 8.0 * N3 * N3 * r3["matvecs"]
         cfg3 = {"workload": f"config3: N={N3} complex double geometric, nev={nev3}, nex={nex3}, deg={DEG}, one subspace "
-                            "iteration (P:727-731), 1x1; 1 warm-up + 1 timed iteration",
+                            "iteration (P:727-731), 1x1; 1 warm-up + 1 timed iteration; FP64 DMMA products",
                 "value": f3 / r3["t_all"] / 1e12, "unit": "TFLOP/s", "ms_per_step": r3["t_all"] * 1e3,
                 "filter_tflops": f3 / r3["t_filter"] / 1e12,
                 "roofline_frac": f3 / r3["t_filter"] / 1e12 / (dmma_peak * 4.0 / 3.0),
@@ -505,7 +544,8 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": dev_s_max / args.steps * 1e3,
-                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "c128",
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+                "dtype": "c128 (products: int8 slices -> int32 -> f64)" if EMU else "c128",
                 "data": f"synthetic (seeded G2 generator: H = Phi P C P^H Phi^H with the Table 1 {args.family} spectrum, d_max=1, eps=1e-4)",
                 "config": {"workload": ({(N1, NEV, NEX): "config2", (60000, 1000, 300): "config3",
                                          (115000, 1200, 400): "config4"}.get((args.n, nev, nex), "custom")
@@ -516,13 +556,12 @@ def main():
                 "wall_ms_per_step": t_wall / args.steps * 1e3,
                 "phases_s_per_step": phases,
                 "filter_tflops_per_gpu": achieved,
-                "roofline": {"bound": "tensor", "achieved": achieved, "peak": dmma_peak * 4.0 / 3.0, "unit": "TFLOP/s",
-                             "frac": achieved / (dmma_peak * 4.0 / 3.0), "traffic": traffic,
-                             "kernel": "zgemm3m_dmma_kernel (filter step: 3M complex product on FP64 DMMA.8x8x4, TMA-staged)",
-                             "per_launch_flops": per_launch_flops, "launches": launches_filter,
-                             "dmma_pipe_frac": achieved * 0.75 / dmma_peak,
-                             "peak_source": f"4/3 x the FP64 DMMA.8x8x4 peak {dmma_peak:.2f} TFLOP/s ({peak_src}): 3M spends 3 real DMMA MACs per complex MAC; MEASURED_PEAKS.json has no FP64 entry"},
+                "roofline": roof,
+                "fp64_products": ("Ozaki-scheme emulation on INT8 tensor cores (7 slices, step error ~1e-14 vs FP64 "
+                                  "DMMA; SURVEY f4)" if EMU else "FP64 DMMA"),
                 "clocks": clocks, "gpu_launches": launches, "e2e": e2e}
+        if other:
+            line["c128_dmma_iteration" if EMU else "c128_ozaki_iteration"] = other
         if tts:
             line["time_to_solution"] = tts
         if c64:

@@ -70,9 +70,19 @@ static ZgemmDesc step_desc(chase_handle* h, int dir, const void* H, int64_t ldh,
 
 // local product of a step: FP64 DMMA GEMM, or (f4, fp64_emulation > 0, complex double) the
 // Ozaki-scheme emulation on the INT8 tensor cores (ozaki.cu)
+// (default, S = 7).  Falls back to DMMA for good when the slices do not fit in device memory, and
+// for K > 133143 (int32-exact accumulation bound; K chunking is not built).
 static void step_gemm(chase_handle* h, const ZgemmDesc& d) {
-  if (h->dtype == CHASE_C128 && h->opt.fp64_emulation > 0 && !d.red) ozaki_step(h, d);
-  else gemm(h, d);
+  if (h->dtype == CHASE_C128 && h->opt.fp64_emulation > 0 && !d.red && !h->oz_off && d.K <= 133143) {
+    try {
+      ozaki_step(h, d);
+      return;
+    } catch (const std::bad_alloc&) {
+      h->oz_off = true;
+      ozaki_release(h);
+    }
+  }
+  gemm(h, d);
 }
 
 void hemm_step(chase_handle* h, int dir, const void* H, int64_t ldh, const void* X, int64_t ldx,
@@ -365,7 +375,18 @@ chase_status guarded(chase_handle* h, F&& f, bool collective = true) {
   return st;
 }
 
+// Derived copies of the caller's shard (Ozaki slices, the c64 lo part, the f4 shadow) are cached
+// by pointer only within one API call: the caller may rewrite H, or free it and get the same
+// address back for a different matrix, between calls.
+void invalidate_shard_caches(chase_handle* h) {
+  h->oz_fwd.src = nullptr;
+  h->oz_bwd.src = nullptr;
+  h->hlo_src = nullptr;
+  h->h32_src = nullptr;
+}
+
 void order_after_user(chase_handle* h) {
+  invalidate_shard_caches(h);
   if (h->user_stream && h->user_stream != h->stream) {
     CHASE_CUDA(cudaEventRecord(h->ev0, h->user_stream));
     CHASE_CUDA(cudaStreamWaitEvent(h->stream, h->ev0, 0));

@@ -79,7 +79,7 @@ struct Options {
   bool fused_reduce_c64 = false;  // f1 for the complex-single filter (measured slower than NCCL + rebuild)
   double peer_timeout = 120.0;    // f1: seconds a rank waits for its peers' tiles before failing
   double comm_timeout = 0.0;      // host waits poll ncclCommGetAsyncError; > 0: also fail after this many s
-  int fp64_emulation = 0;         // f4: > 0 = complex-double filter products on INT8 tensor cores (Ozaki, S slices)
+  int fp64_emulation = 7;         // f4: > 0 = complex-double filter products on INT8 tensor cores (Ozaki, S slices)
 };
 
 }  // namespace chase
@@ -111,7 +111,8 @@ struct chase_handle {
     int S = 0;
     chase::DBuf slices, exps, diag;
   } oz_fwd, oz_bwd;
-  chase::DBuf oz_b, oz_t;              // fp64_emulation: slices of the block X, FP64 product accumulators
+  bool oz_off = false;                 // fp64_emulation fell back to DMMA (slices did not fit)
+  chase::DBuf oz_b, oz_t, oz_sync;     // fp64_emulation: slices of the block X, FP64 product accumulators
   const void* h32_src = nullptr;
   int64_t h32_ld = 0;
   const void* hlo_src = nullptr;

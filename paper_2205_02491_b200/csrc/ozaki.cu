@@ -31,6 +31,7 @@
 // step epilogue  Y = alpha (C - gamma E X) + beta Y.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <type_traits>
 #include <vector>
@@ -57,6 +58,8 @@ struct Params {
   double* out;                         // FP64 accumulator of the real product (M x N, ld ldo)
   int64_t ldo;
   int accumulate;                      // 0: out = scale acc; 1: out += scale acc
+  int hint;                            // 1: L2 evict_first for A (streamed), evict_last for B (re-read)
+  unsigned* sync;                      // round barrier counter (zeroed per launch); null = no barrier
 };
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {   // K-major, SWIZZLE_128B, 8-row groups 1 KB apart
@@ -85,6 +88,13 @@ __device__ __forceinline__ void tma_3d_pair(uint32_t dst, const CUtensorMap* m, 
   asm volatile(
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d_pair_hint(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -122,9 +132,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + 2 * BM - 1) / (2 * BM);
-  const int T = tiles_n * tiles_m;
   const int pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
   const int KT = (p.K + BK - 1) / BK;
+  // Static L2-aware schedule: the pairs form groups of tiles_n; group g walks the m tiles
+  // g, g + ngroups, ... and pair j of the group always takes n tile j, so the tiles_n pairs that
+  // read one A panel run it in lockstep and share it through L2 (a round-robin walk lets them
+  // drift apart: measured 13x the A traffic at 12 n tiles).  Pairs beyond ngroups x tiles_n idle.
+  const bool grouped = tiles_n <= npair;
+  const int ngroups = grouped ? npair / tiles_n : 1;
+  const int g = pair / tiles_n, jn = pair % tiles_n;
+  const bool active = !grouped || g < ngroups;
+  // tile r of this pair: (m tile, n tile); ntile() = number of tiles
+  auto ntile = [&]() -> int {
+    if (!active) return 0;
+    if (grouped) return g < tiles_m ? (tiles_m - 1 - g) / ngroups + 1 : 0;
+    const int T = tiles_n * tiles_m;
+    return pair < T ? (T - 1 - pair) / npair + 1 : 0;
+  };
+  auto tile_mn = [&](int r, int& tmi, int& tni) {
+    if (grouped) { tmi = g + r * ngroups; tni = jn; }
+    else { const int t = pair + r * npair; tmi = t / tiles_n; tni = t % tiles_n; }
+  };
+  const int NT = ntile();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -151,10 +180,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       tma_prefetch_desc(&tA);
       tma_prefetch_desc(&tB);
+      uint64_t pol_a = 0, pol_b = 0;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
       int it = 0;
-      for (int t = pair; t < T; t += npair) {
-        const int m0 = (t / tiles_n) * 2 * BM + (int)rank * BM;
-        const int nh = (t % tiles_n) * BN + (int)rank * (BN / 2);
+      unsigned target = 0;
+      for (int r = 0; r < NT; ++r) {
+        if (p.sync && grouped && r > 0) {
+          // Round barrier of the producers (performance only): every CTA starts loading round r
+          // together, so the pairs stream the A and B k windows in step and share them through L2
+          // (B, re-read by every m round, does not fit L2; without the barrier the pairs drift
+          // apart over a launch -- measured 35 GB vs 13 GB of DRAM reads per launch).  The
+          // results never depend on it: a CTA that waits longer than 200 us (e.g. not all CTAs
+          // resident because another kernel shares the GPU) stops synchronising and carries on.
+          target += 2u * (unsigned)tiles_n * (unsigned)min(ngroups, tiles_m - r * ngroups);
+          atomicAdd(p.sync, 1u);
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          unsigned v;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync) : "memory");
+            if (v >= target) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 200000ull) { p.sync = nullptr; break; }
+          }
+        }
+        int tmi, tni;
+        tile_mn(r, tmi, tni);
+        const int m0 = tmi * 2 * BM + (int)rank * BM;
+        const int nh = tni * BN + (int)rank * (BN / 2);
         for (int kt = 0; kt < KT; ++kt) {
           for (int q = 0; q < p.npairs; ++q, ++it) {
             const int s = it % STAGES;
@@ -162,8 +216,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
             const uint32_t fb = mapa0(smem_u32(full + s));
             if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * STAGE_BYTES);
-            tma_3d_pair(st, &tA, kt * BK, m0, p.sa[q], fb);
-            tma_3d_pair(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb);
+            if (p.hint) {
+              tma_3d_pair_hint(st, &tA, kt * BK, m0, p.sa[q], fb, pol_a);
+              tma_3d_pair_hint(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb, pol_b);
+            } else {
+              tma_3d_pair(st, &tA, kt * BK, m0, p.sa[q], fb);
+              tma_3d_pair(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb);
+            }
           }
         }
       }
@@ -176,7 +235,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)((2 * BM) >> 4) << 24);
       int it = 0, tl = 0;
-      for (int t = pair; t < T; t += npair, ++tl) {
+      for (int r = 0; r < NT; ++r, ++tl) {
         const int b = tl & 1;
         if (tl >= 2) {
           wait_cluster(acc_empty + b, ((tl >> 1) - 1) & 1);
@@ -208,10 +267,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int quad = warp & 3;
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     int tl = 0;
-    for (int t = pair; t < T; t += npair, ++tl) {
+    for (int r = 0; r < NT; ++r, ++tl) {
       const int b = tl & 1;
-      const int row = (t / tiles_n) * 2 * BM + (int)rank * BM + 32 * quad + lane;
-      const int n0 = (t % tiles_n) * BN;
+      int tmi, tni;
+      tile_mn(r, tmi, tni);
+      const int row = tmi * 2 * BM + (int)rank * BM + 32 * quad + lane;
+      const int n0 = tni * BN;
       mbar_wait(acc_full + b, (tl >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t base = tm + lane_off + (uint32_t)b * BN;
@@ -570,7 +631,12 @@ void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
   const int lines_a = M;
   const int64_t ldka = oz::ldk_of(K);
   // pairs per int32 accumulator: npairs 127^2 K <= 2^31 - 1 (exact accumulation)
-  const int cap = (int)std::max<int64_t>(1, std::min<int64_t>(oz::MAX_PAIRS, 2147483647LL / (16129LL * K)));
+  int cap = (int)std::max<int64_t>(1, std::min<int64_t>(oz::MAX_PAIRS, 2147483647LL / (16129LL * K)));
+  static const int cap_env = [] { const char* e = std::getenv("CHASE_OZ_PAIRS"); return e ? std::atoi(e) : 0; }();
+  if (cap_env > 0) cap = std::min(cap, cap_env);          // tuning knob: slice pairs per launch
+  static const int hint_env = [] { const char* e = std::getenv("CHASE_OZ_HINT"); return e ? std::atoi(e) : 0; }();
+  static const int sync_env = [] { const char* e = std::getenv("CHASE_OZ_SYNC"); return e ? std::atoi(e) : 1; }();
+  h->oz_sync.alloc(256);
   if (16129LL * K > 2147483647LL) throw UsageError("fp64_emulation: K > 133143 needs K chunking (not built)");
   const int ptiles = ceil_div(M, 2 * oz::BM) * ceil_div(N, oz::BN);
   int sms = 148;
@@ -601,6 +667,12 @@ void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
         prm.out = T + (size_t)P * M * N;
         prm.ldo = M;
         prm.accumulate = first ? 0 : 1;
+        prm.hint = hint_env;
+        prm.sync = nullptr;
+        if (sync_env) {
+          CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, st));
+          prm.sync = h->oz_sync.as<unsigned>();
+        }
         first = false;
         oz::oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(ta, tb, prm);
         CHASE_CHECK_LAUNCH();
@@ -634,6 +706,7 @@ void ozaki_release(chase_handle* h) {
   }
   h->oz_b.release();
   h->oz_t.release();
+  h->oz_sync.release();
 }
 
 }  // namespace chase

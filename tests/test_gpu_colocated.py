@@ -24,6 +24,9 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 GRIDS = [(1, 2), (2, 2), (2, 4)]
+# c128-fused: FP64 DMMA steps with the f1 epilogue reduction; c128-allreduce: the default complex-
+# double path (Ozaki INT8 emulation of the FP64 products, fp64_emulation = 7) with the pipelined
+# all-reduce
 MODES = ["c128-fused", "c128-allreduce", "r64-fused", "r64-allreduce", "c64-fused", "c64-allreduce"]
 NEV, NEX = 40, 20
 
@@ -96,6 +99,8 @@ def test_colocated_grid(grid, mode, capfd, monkeypatch):
                 ch.set_option("fused_reduce", 0)
             elif single:
                 ch.set_option("fused_reduce_c64", 1)
+            else:
+                ch.set_option("fp64_emulation", 0)      # the fused epilogue lives in the DMMA kernels
             dH = _dev(H[r0:r0 + p, c0:c0 + q], hdt)
             out = {"r0": r0, "p": p, "c0": c0, "q": q, "i": rank % grid[0], "j": rank // grid[0]}
             # a2 + a3: forward step, W-layout rows [r0, r0+p)

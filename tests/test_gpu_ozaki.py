@@ -96,3 +96,25 @@ def test_emulated_filter_and_solve():
     assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
     Vv = vecs.cpu().numpy()[:, :nev]
     assert np.max(np.linalg.norm(H @ Vv - Vv * vals[None, :], axis=0)) <= 1e-10 * normH
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_shard_rewritten_in_place_is_resliced(dtype):
+    """Derived copies of the shard (Ozaki slices; the c64 3xTF32 lo part) are rebuilt on every API
+    call: rewriting H in place (same pointer) between calls must change the result."""
+    import paper_2205_02491_b200 as pkg
+    N, n = 512, 16
+    cdt = np.complex64 if dtype == "c64" else np.complex128
+    H1 = make_matrix("uniform", N, "g2", seed=1).dense().astype(cdt)
+    H2 = make_matrix("wilkinson", N, "g2", seed=2).dense().astype(cdt)
+    rng = np.random.default_rng(0)
+    X = (rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))).astype(cdt)
+    ch = pkg.Chase(N, n, 1, dtype=dtype)
+    dH, dX = _dev(H1), _dev(X)
+    tol = 1e-5 if dtype == "c64" else 1e-13
+    for H in (H1, H2):
+        dH.copy_(torch.from_numpy(np.asfortranarray(H)))
+        dY = _dev(np.zeros((N, n), dtype=cdt))
+        ch.hemm_step(0, dH, dX, dY, n, 1.0, 0.0, 0.0)
+        ref = H.astype(complex) @ X.astype(complex)
+        assert _rel(dY.cpu().numpy().astype(complex), ref) <= tol

@@ -40,6 +40,7 @@ def filter_coloc():
             ch = pkg.Chase(N, 4, 4, grid=grid, rank=rank, world_size=4, nccl_id=key, colocated=True)
             try:
                 ch.set_option("fused_reduce", fused)
+                ch.set_option("fp64_emulation", 0)
                 dV = dev(V[c0:c0 + q])
                 dW = dev(np.zeros((p, 4), dtype=complex))
                 ch.filter(dev(H[r0:r0 + p, c0:c0 + q]), dV, dW, degrees, M.lam[-1] * 1.01, M.lam[0], M.lam[40])

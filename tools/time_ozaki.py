@@ -23,6 +23,7 @@ g = torch.Generator(device="cuda").manual_seed(0)
 X = torch.randn((n, N), dtype=torch.complex128, device="cuda", generator=g).t()
 Y0 = torch.randn((n, N), dtype=torch.complex128, device="cuda", generator=g).t()
 ch = pkg.Chase(N, n, 1)
+ch.set_option("fp64_emulation", 0)            # DMMA reference first
 
 
 def run(direction, reps=3):
