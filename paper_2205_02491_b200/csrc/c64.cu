@@ -188,6 +188,31 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
         CHASE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
       kern<<<grid2, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P);
     };
+    static const bool persistent = !getenv("CHASE_C64_PERSIST") || atoi(getenv("CHASE_C64_PERSIST")) != 0;
+    if (!red && persistent) {
+      // persistent grouped schedule with the L2 round barrier (cgemm_tc.cuh c64_step_kernel_p)
+      static unsigned long long attrp[2] = {0, 0};
+      int sms = 148, dev = 0;
+      CHASE_CUDA(cudaGetDevice(&dev));
+      CHASE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const int ptiles = ceil_div(P.M, 2 * BMR) * ceil_div(P.N, BN);
+      const int gridp = 2 * std::min(ptiles, sms / 2);
+      static const int gw_env = getenv("CHASE_C64_GW") ? atoi(getenv("CHASE_C64_GW")) : 0;
+      const int tiles_n = ceil_div(P.N, BN);
+      int gw = c64_segment_width(tiles_n, gridp / 2);
+      if (gw_env > 0 && tiles_n % gw_env == 0 && gw_env <= gridp / 2) gw = gw_env;   // tuning knob
+      h->oz_sync.alloc(256);
+      CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, h->stream));
+      unsigned* sy = h->oz_sync.as<unsigned>();
+      auto gp = [&](auto kern, int slot) {
+        if (first_on_device(attrp[slot]))
+          CHASE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
+        kern<<<gridp, C64_THREADS, SMEM2, h->stream>>>(ta, tal, tb1, tb1l, tb2, tb2l, P, sy, gw);
+      };
+      if (dir == 0) gp(c64_step_kernel_p<true, BN>, 0); else gp(c64_step_kernel_p<false, BN>, 1);
+      CHASE_CHECK_LAUNCH();
+      return;
+    }
     if (dir == 0) {
       if (red) go(c64_step_kernel2<true, BN, true>, 0); else go(c64_step_kernel2<true, BN, false>, 1);
     } else {

@@ -664,4 +664,226 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(TCOLS));
 }
 
+// ============================================================================================
+// Persistent CTA-pair variant (the default, no fused reduction).  L2-aware static schedule: the
+// n tiles are cut into segments of gw (a divisor of tiles_n chosen on the host so that a round's
+// a x gw tile block, a = npair / gw, reads the fewest A and B panels per tile); the pairs form
+// a = npair / gw groups of gw, group g walks the m tiles g, g + a, ... of segment 0, then of
+// segment 1, ..., and pair j of the group always takes n tile seg gw + j.  The gw pairs of a group
+// stream one A panel (the big H shard) in lockstep, and a round barrier of the TMA producers
+// (200 us timeout: performance only, never correctness) keeps the groups in step, so the B panels
+// of the segment are shared too.  (Panels are K long -- far beyond L2 at large shards -- so a
+// round costs a + gw panel reads: 17 for 8 x 9 vs 34 for 2 x 32 at N = 170000 / 2 x 2.)  The chunk
+// accumulators stay double-buffered across tiles (global chunk counter), so the next tile's first
+// chunk overlaps this tile's epilogue.  sync: round-barrier counter (zeroed per launch) or null.
+template <bool FWD, int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
+    c64_step_kernel_p(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tAlo,
+                      const __grid_constant__ CUtensorMap tB1, const __grid_constant__ CUtensorMap tB1lo,
+                      const __grid_constant__ CUtensorMap tB2, const __grid_constant__ CUtensorMap tB2lo,
+                      C64Params p, unsigned* sync, int gw) {
+  using namespace tc;
+  constexpr uint32_t B_BYTES = Cfg2<BN>::B_BYTES, STAGE_BYTES = Cfg2<BN>::STAGE_BYTES;
+  constexpr int STAGES = Cfg2<BN>::STAGES;
+  const int CH = p.kc_stages > 0 ? p.kc_stages : C64_KC_STAGES;
+  constexpr uint32_t TCOLS = 4 * BN;
+  constexpr int HN = BN / 2;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc2::cluster_rank();
+  const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + 2 * BMR - 1) / (2 * BMR);
+  const int pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
+  const int nseg = tiles_n / gw, ngroups = npair / gw;
+  const int g = pair / gw, jn = pair % gw;
+  // m tiles of group gg per segment, and this pair's tile count
+  auto cnt = [&](int gg) { return gg < tiles_m ? (tiles_m - 1 - gg) / ngroups + 1 : 0; };
+  const int NT = g < ngroups ? nseg * cnt(g) : 0;
+  auto tile_mn = [&](int r, int& tmi, int& tni) {
+    const int c = cnt(g);
+    tmi = g + (r % c) * ngroups;
+    tni = (r / c) * gw + jn;
+  };
+  const int KT = (p.K + BK - 1) / BK;
+  const int NCH = (KT + CH - 1) / CH;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 16);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  tc2::cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tA);
+      tma_prefetch_desc(rank == 0 ? &tB1 : &tB2);
+      const CUtensorMap* tb = rank == 0 ? &tB1 : &tB2;
+      const CUtensorMap* tbl = rank == 0 ? &tB1lo : &tB2lo;
+      int it = 0;
+      unsigned target = 0;
+      for (int r = 0; r < NT; ++r) {
+        if (sync && r > 0) {
+          // arrivals at round r: the CTAs of the groups that still have an r-th tile
+          int act = 0;
+          for (int gg = 0; gg < ngroups; ++gg) act += (nseg * cnt(gg) > r) ? 1 : 0;
+          target += 2u * (unsigned)gw * (unsigned)act;
+          atomicAdd(sync, 1u);
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          unsigned v;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sync) : "memory");
+            if (v >= target) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 200000ull) { sync = nullptr; break; }
+          }
+        }
+        int tmi, tni;
+        tile_mn(r, tmi, tni);
+        const int m0 = tmi * (2 * BMR) + (int)rank * BMR;
+        const int n0 = tni * BN;
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(empty + s, ((it / STAGES) - 1) & 1);
+          const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+          const uint32_t fb = tc2::mapa(smem_u32(full + s), 0);
+          if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * STAGE_BYTES);
+          const int k0 = kt * BK;
+          if constexpr (FWD) {
+#pragma unroll
+            for (int c = 0; c < BMR / 32; ++c) {
+              tc2::tma_load_2d_pair(st + c * (BK * 128), &tA, m0 + 32 * c, k0, fb);
+              tc2::tma_load_2d_pair(st + A_BYTES + c * (BK * 128), &tAlo, m0 + 32 * c, k0, fb);
+            }
+          } else {
+            tc2::tma_load_2d_pair(st, &tA, k0, m0, fb);
+            tc2::tma_load_2d_pair(st + A_BYTES, &tAlo, k0, m0, fb);
+          }
+          tc2::tma_load_2d_pair(st + 2 * A_BYTES, tb, k0, n0, fb);
+          tc2::tma_load_2d_pair(st + 2 * A_BYTES + B_BYTES, tbl, k0, n0, fb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      uint32_t leader;
+      asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((FWD ? 1u : 0u) << 15) |
+                             ((uint32_t)((2 * BN) >> 3) << 17) | ((uint32_t)((2 * BMR) >> 4) << 24);
+      int it = 0, gc = 0;
+      for (int r = 0; r < NT; ++r) {
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int s = it % STAGES;
+          const bool chunk_start = (kt % CH) == 0;
+          const int cg = gc + kt / CH, b = cg & 1;            // global chunk index
+          if (chunk_start && cg >= 2) {
+            tc2::wait_cluster(acc_empty + b, ((cg >> 1) - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+          }
+          mbar_wait(full + s, (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (leader) {
+            const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
+            const uint32_t sa = st, salo = st + A_BYTES, sb = st + 2 * A_BYTES;
+            const uint32_t td = tm + (uint32_t)b * 2 * BN;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              uint64_t da, dal;
+              if constexpr (FWD) {
+                da = sdesc(sa + kk * 1024, BK * 128, 512, 1);
+                dal = sdesc(salo + kk * 1024, BK * 128, 512, 1);
+              } else {
+                da = sdesc(sa + kk * 32, 16, 1024, 2);
+                dal = sdesc(salo + kk * 32, 16, 1024, 2);
+              }
+              const uint64_t db = sdesc(sb + kk * 32, 16, 1024, 2);
+              const uint64_t dbl = sdesc(sb + B_BYTES + kk * 32, 16, 1024, 2);
+              const uint32_t acc = (chunk_start && kk == 0) ? 0u : 1u;
+              tc2::mma_tf32(td, da, db, idesc, acc);
+              tc2::mma_tf32(td, da, dbl, idesc, 1u);
+              tc2::mma_tf32(td, dal, db, idesc, 1u);
+            }
+            tc2::commit_both(empty + s);
+            if ((kt % CH) == CH - 1 || kt == KT - 1) tc2::commit_both(acc_full + b);
+          }
+          __syncwarp();
+        }
+        gc += NCH;
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int gc = 0;
+    for (int r = 0; r < NT; ++r) {
+      int tmi, tni;
+      tile_mn(r, tmi, tni);
+      const int m0 = tmi * (2 * BMR) + (int)rank * BMR;
+      const int n0 = tni * BN;
+      const int row = m0 + 32 * quad + lane;
+      const uint32_t lane_base = tm + ((uint32_t)(32 * quad) << 16) + (uint32_t)(half * HN);
+      float a1[HN], a2[HN];
+#pragma unroll
+      for (int j = 0; j < HN; ++j) a1[j] = a2[j] = 0.f;
+      for (int chunk = 0; chunk < NCH; ++chunk, ++gc) {
+        const int b = gc & 1;
+        mbar_wait(acc_full + b, (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t base = lane_base + (uint32_t)b * 2 * BN;
+#pragma unroll
+        for (int c0 = 0; c0 < HN; c0 += 16) {
+          uint32_t r1[16], r2[16];
+          tc::ld16(base + c0, r1);
+          tc::ld16(base + BN + c0, r2);
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            a1[c0 + j] += __uint_as_float(r1[j]);
+            a2[c0 + j] += __uint_as_float(r2[j]);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) tc2::arrive_cluster(tc2::mapa(smem_u32(acc_empty + b), 0));
+      }
+      c64_epilogue<FWD, HN>(p, row, n0 + half * HN, a1, a2);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  tc2::cluster_sync();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(TCOLS));
+}
+
+// Segment width of the persistent schedule: the divisor gw of tiles_n (gw <= npair) with the fewest
+// panel reads per tile of a round, (gw + npair / gw) / ((npair / gw) gw).
+inline int c64_segment_width(int tiles_n, int npair) {
+  int best = 1;
+  double bc = 1e30;
+  for (int d = 1; d <= tiles_n && d <= npair; ++d) {
+    if (tiles_n % d) continue;
+    const int a = npair / d;
+    const double c = (double)(d + a) / (double)(a * d);
+    if (c < bc - 1e-12) { bc = c; best = d; }
+  }
+  return best;
+}
+
 }  // namespace chase
+

@@ -73,7 +73,7 @@ static ZgemmDesc step_desc(chase_handle* h, int dir, const void* H, int64_t ldh,
 // (default, S = 7).  Falls back to DMMA for good when the slices do not fit in device memory, and
 // for K > 133143 (int32-exact accumulation bound; K chunking is not built).
 static void step_gemm(chase_handle* h, const ZgemmDesc& d) {
-  if (h->dtype == CHASE_C128 && h->opt.fp64_emulation > 0 && !d.red && !h->oz_off && d.K <= 133143) {
+  if (!h->c64() && h->opt.fp64_emulation > 0 && !d.red && !h->oz_off && d.K <= 133143) {
     try {
       ozaki_step(h, d);
       return;

@@ -335,179 +335,215 @@ __device__ __forceinline__ void cut(double v, int8_t (&a)[S]) {
   }
 }
 
-// Lines contiguous in memory (columns of a column-major complex matrix): line c of `rows`
-// complex values at X + c ld.  Writes, for P in {re, im (negated if conj), re + im}, slices
-// out[(P S + s) * plane + c * ldk + k] and exponents e[P * lines + c].  One CTA per line.
+// The NP real matrices the products run on: complex (NP = 3, Gauss's 3M): re, im (negated if
+// conj), re + im; real symmetric (NP = 1): the value itself.
+template <class T> struct Comp;
+template <> struct Comp<double2> {
+  static constexpr int NP = 3;
+  __device__ static void get(double2 v, double sg, double (&c)[3]) {
+    const double im = sg * v.y;
+    c[0] = v.x;
+    c[1] = im;
+    c[2] = v.x + im;
+  }
+  __device__ static double2 zero() { return make_double2(0.0, 0.0); }
+};
+template <> struct Comp<double> {
+  static constexpr int NP = 1;
+  __device__ static void get(double v, double, double (&c)[1]) { c[0] = v; }
+  __device__ static double zero() { return 0.0; }
+};
+
+// Lines contiguous in memory (columns of a column-major matrix): line c of `rows` values at
+// X + c ld.  Writes, for every real component P (Comp), slices out[(P S + s) * plane + c * ldk + k]
+// and exponents e[P * lines + c].  One CTA per line.
 // diag != INT_MIN: the element k = c + diag of line c lies on the global diagonal of H; it is left
 // out of the slices (zero) and added exactly in FP64 by oz_combine (diagonal split: the dominant
 // diagonal of a Hermitian H would otherwise set the line's exponent and cost the off-diagonal
 // entries their low bits).
-template <int S>
-__global__ void __launch_bounds__(256) oz_slice_lines(const double2* X, int64_t ld, int rows, int lines, int conj,
+template <int S, class T>
+__global__ void __launch_bounds__(256) oz_slice_lines(const T* X, int64_t ld, int rows, int lines, int conj,
                                                       int diag, int8_t* out, int64_t ldk, int64_t plane, int* e) {
+  constexpr int NP = Comp<T>::NP;
   const int c = blockIdx.x;
-  const double2* x = X + (int64_t)c * ld;
+  const T* x = X + (int64_t)c * ld;
   const double sg = conj ? -1.0 : 1.0;
   const int kd = diag == INT_MIN ? -1 : c + diag;
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  double mx[NP];
+#pragma unroll
+  for (int P = 0; P < NP; ++P) mx[P] = 0.0;
   for (int k = threadIdx.x; k < rows; k += 256) {
     if (k == kd) continue;
-    const double2 v = x[k];
-    m0 = fmax(m0, fabs(v.x));
-    m1 = fmax(m1, fabs(v.y));
-    m2 = fmax(m2, fabs(v.x + sg * v.y));
-  }
-  __shared__ double sm[3][8];
+    double v[NP];
+    Comp<T>::get(x[k], sg, v);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-    m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-    m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+    for (int P = 0; P < NP; ++P) mx[P] = fmax(mx[P], fabs(v[P]));
   }
-  if ((threadIdx.x & 31) == 0) {
-    sm[0][threadIdx.x >> 5] = m0;
-    sm[1][threadIdx.x >> 5] = m1;
-    sm[2][threadIdx.x >> 5] = m2;
+  __shared__ double sm[NP][8];
+#pragma unroll
+  for (int P = 0; P < NP; ++P) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx[P] = fmax(mx[P], __shfl_xor_sync(0xffffffffu, mx[P], o));
+    if ((threadIdx.x & 31) == 0) sm[P][threadIdx.x >> 5] = mx[P];
   }
   __syncthreads();
-  __shared__ int ex[3];
-  if (threadIdx.x < 3) {
+  __shared__ int ex[NP];
+  if (threadIdx.x < NP) {
     double m = 0.0;
     for (int w = 0; w < 8; ++w) m = fmax(m, sm[threadIdx.x][w]);
     ex[threadIdx.x] = line_exp(m);
     e[threadIdx.x * lines + c] = ex[threadIdx.x];
   }
   __syncthreads();
-  const double sc0 = ldexp(1.0, -ex[0]), sc1 = ldexp(1.0, -ex[1]), sc2 = ldexp(1.0, -ex[2]);
+  double sc[NP];
+#pragma unroll
+  for (int P = 0; P < NP; ++P) sc[P] = ldexp(1.0, -ex[P]);
   for (int k = threadIdx.x; k < (int)ldk; k += 256) {
-    int8_t a0[S], a1[S], a2[S];
+    int8_t a[NP][S];
+    double v[NP];
     if (k < rows && k != kd) {
-      const double2 v = x[k];
-      const double im = sg * v.y;
-      cut<S>(v.x * sc0, a0);
-      cut<S>(im * sc1, a1);
-      cut<S>((v.x + im) * sc2, a2);
+      Comp<T>::get(x[k], sg, v);
     } else {
 #pragma unroll
-      for (int s = 0; s < S; ++s) a0[s] = a1[s] = a2[s] = 0;
+      for (int P = 0; P < NP; ++P) v[P] = 0.0;
     }
+#pragma unroll
+    for (int P = 0; P < NP; ++P) cut<S>(v[P] * sc[P], a[P]);
     int8_t* o = out + (int64_t)c * ldk + k;
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      o[(int64_t)(0 * S + s) * plane] = a0[s];
-      o[(int64_t)(1 * S + s) * plane] = a1[s];
-      o[(int64_t)(2 * S + s) * plane] = a2[s];
-    }
+    for (int P = 0; P < NP; ++P)
+#pragma unroll
+      for (int s = 0; s < S; ++s) o[(int64_t)(P * S + s) * plane] = a[P][s];
   }
 }
 
-// Row maxima of a column-major complex matrix (rows of H for the forward A operand): |re|,
-// |im|, |re + im| per row, as order-preserving bit patterns (non-negative doubles) via atomicMax.
-__global__ void oz_row_max(const double2* H, int64_t ld, int rows, int cols, int diag, unsigned long long* mx) {
+// Row maxima (rows of H for the forward A operand) per real component, as order-preserving bit
+// patterns of non-negative doubles via atomicMax.
+template <class T>
+__global__ void oz_row_max(const T* H, int64_t ld, int rows, int cols, int diag, unsigned long long* mx) {
+  constexpr int NP = Comp<T>::NP;
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= rows) return;
   const int c0 = blockIdx.y * 256, c1 = min(cols, c0 + 256);
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  double m[NP];
+#pragma unroll
+  for (int P = 0; P < NP; ++P) m[P] = 0.0;
   for (int j = c0; j < c1; ++j) {
     if (j == i + diag) continue;                      // diagonal split (see oz_slice_lines)
-    const double2 v = H[i + (int64_t)j * ld];
-    m0 = fmax(m0, fabs(v.x));
-    m1 = fmax(m1, fabs(v.y));
-    m2 = fmax(m2, fabs(v.x + v.y));
+    double v[NP];
+    Comp<T>::get(H[i + (int64_t)j * ld], 1.0, v);
+#pragma unroll
+    for (int P = 0; P < NP; ++P) m[P] = fmax(m[P], fabs(v[P]));
   }
-  atomicMax(mx + i, (unsigned long long)__double_as_longlong(m0));
-  atomicMax(mx + rows + i, (unsigned long long)__double_as_longlong(m1));
-  atomicMax(mx + 2 * rows + i, (unsigned long long)__double_as_longlong(m2));
+#pragma unroll
+  for (int P = 0; P < NP; ++P) atomicMax(mx + P * rows + i, (unsigned long long)__double_as_longlong(m[P]));
 }
 
 // Transposing slicer for the forward A operand: row i of H (strided) -> line i of the output
 // (contiguous in k = column index j).  Tile of 32 rows x 64 columns through shared memory.
-template <int S>
-__global__ void __launch_bounds__(256) oz_slice_rows(const double2* H, int64_t ld, int rows, int cols, int diag,
+template <int S, class T>
+__global__ void __launch_bounds__(256) oz_slice_rows(const T* H, int64_t ld, int rows, int cols, int diag,
                                                      const unsigned long long* mx, int8_t* out, int64_t ldk,
                                                      int64_t plane, int* e) {
-  __shared__ double2 t[64][33];
+  constexpr int NP = Comp<T>::NP;
+  __shared__ T t[64][33];
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 64;
   for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
     const int ii = idx & 31, jj = idx >> 5;
     const int i = i0 + ii, j = j0 + jj;
-    t[jj][ii] = (i < rows && j < cols && j != i + diag) ? H[i + (int64_t)j * ld] : make_double2(0.0, 0.0);
+    t[jj][ii] = (i < rows && j < cols && j != i + diag) ? H[i + (int64_t)j * ld] : Comp<T>::zero();
   }
   __syncthreads();
   // thread -> (row ii, 8-column group): 8 consecutive k per slice
   const int ii = threadIdx.x >> 3, jg = (threadIdx.x & 7) * 8;
   const int i = i0 + ii;
   if (i >= rows) return;
-  int ex[3];
+  int ex[NP];
+  double sc[NP];
 #pragma unroll
-  for (int P = 0; P < 3; ++P) ex[P] = line_exp(__longlong_as_double((long long)mx[P * rows + i]));
+  for (int P = 0; P < NP; ++P) {
+    ex[P] = line_exp(__longlong_as_double((long long)mx[P * rows + i]));
+    sc[P] = ldexp(1.0, -ex[P]);
+  }
   if (blockIdx.y == 0 && (threadIdx.x & 7) == 0) {
 #pragma unroll
-    for (int P = 0; P < 3; ++P) e[P * rows + i] = ex[P];
+    for (int P = 0; P < NP; ++P) e[P * rows + i] = ex[P];
   }
-  const double sc0 = ldexp(1.0, -ex[0]), sc1 = ldexp(1.0, -ex[1]), sc2 = ldexp(1.0, -ex[2]);
 #pragma unroll 1
   for (int jj = 0; jj < 8; ++jj) {
     const int j = j0 + jg + jj;
     if (j >= (int)ldk) break;
-    const double2 v = t[jg + jj][ii];
-    int8_t a0[S], a1[S], a2[S];
-    cut<S>(v.x * sc0, a0);
-    cut<S>(v.y * sc1, a1);
-    cut<S>((v.x + v.y) * sc2, a2);
+    double v[NP];
+    Comp<T>::get(t[jg + jj][ii], 1.0, v);
+    int8_t a[NP][S];
+#pragma unroll
+    for (int P = 0; P < NP; ++P) cut<S>(v[P] * sc[P], a[P]);
     int8_t* o = out + (int64_t)i * ldk + j;
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      o[(int64_t)(0 * S + s) * plane] = a0[s];
-      o[(int64_t)(1 * S + s) * plane] = a1[s];
-      o[(int64_t)(2 * S + s) * plane] = a2[s];
-    }
+    for (int P = 0; P < NP; ++P)
+#pragma unroll
+      for (int s = 0; s < S; ++s) o[(int64_t)(P * S + s) * plane] = a[P][s];
   }
 }
 
-// Y = alpha (C - gamma E X) + beta Y from the three FP64 real products (3M) with their exponents
-// rows m in [dlo, dhi) carry the diagonal split and the shift: + alpha (hdiag[m] - gamma) X[m + doff]
-__global__ void oz_combine(const double* T, int64_t ldt, int64_t tplane, const int* eA, int M, const int* fB, int N,
-                           double2* Y, int64_t ldy, double alpha, double beta, int beta_on, const double2* X,
-                           int64_t ldx, const double2* hdiag, int dlo, int dhi, int64_t doff, double gamma) {
+// Y = alpha (C - gamma E X) + beta Y from the FP64 real products with their exponents (complex:
+// the three products of 3M, Re C = T1 - T2, Im C = T3 - T1 - T2; real: C = T1).  Rows m in
+// [dlo, dhi) carry the diagonal split and the shift: + alpha (hdiag[m] - gamma) X[m + doff].
+__device__ __forceinline__ double2 c_fma(double a, double2 v, double2 acc) {
+  return make_double2(acc.x + a * v.x, acc.y + a * v.y);
+}
+template <class T>
+__global__ void oz_combine(const double* T_, int64_t ldt, int64_t tplane, const int* eA, int M, const int* fB, int N,
+                           T* Y, int64_t ldy, double alpha, double beta, int beta_on, const T* X, int64_t ldx,
+                           const double2* hdiag, int dlo, int dhi, int64_t doff, double gamma) {
   const int64_t total = (int64_t)M * N;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int m = (int)(idx % M), n = (int)(idx / M);
     const int64_t o = (int64_t)m + (int64_t)n * ldt;
-    const double t1 = ldexp(T[o], eA[m] + fB[n]);
-    const double t2 = ldexp(T[tplane + o], eA[M + m] + fB[N + n]);
-    const double t3 = ldexp(T[2 * tplane + o], eA[2 * M + m] + fB[2 * N + n]);
-    double re = alpha * (t1 - t2), im = alpha * (t3 - t1 - t2);
-    if (m >= dlo && m < dhi) {
-      const double2 x = X[(int64_t)m + doff + (int64_t)n * ldx];
-      const double2 hd = hdiag[m];
-      const double dr = hd.x - gamma;
-      re += alpha * (dr * x.x - hd.y * x.y);
-      im += alpha * (dr * x.y + hd.y * x.x);
+    T* y = Y + (int64_t)m + (int64_t)n * ldy;
+    const double t1 = ldexp(T_[o], eA[m] + fB[n]);
+    if constexpr (Comp<T>::NP == 3) {
+      const double t2 = ldexp(T_[tplane + o], eA[M + m] + fB[N + n]);
+      const double t3 = ldexp(T_[2 * tplane + o], eA[2 * M + m] + fB[2 * N + n]);
+      double re = alpha * (t1 - t2), im = alpha * (t3 - t1 - t2);
+      if (m >= dlo && m < dhi) {
+        const double2 x = X[(int64_t)m + doff + (int64_t)n * ldx];
+        const double2 hd = hdiag[m];
+        const double dr = hd.x - gamma;
+        re += alpha * (dr * x.x - hd.y * x.y);
+        im += alpha * (dr * x.y + hd.y * x.x);
+      }
+      if (beta_on) {
+        const double2 yo = *y;
+        re += beta * yo.x;
+        im += beta * yo.y;
+      }
+      *y = make_double2(re, im);
+    } else {
+      double v = alpha * t1;
+      if (m >= dlo && m < dhi) v += alpha * (hdiag[m].x - gamma) * X[(int64_t)m + doff + (int64_t)n * ldx];
+      if (beta_on) v += beta * *y;
+      *y = v;
     }
-    double2* y = Y + (int64_t)m + (int64_t)n * ldy;
-    if (beta_on) {
-      const double2 yo = *y;
-      re += beta * yo.x;
-      im += beta * yo.y;
-    }
-    *y = make_double2(re, im);
   }
 }
 
 // the diagonal element of output row m (forward: H[m][m + off]; backward: conj(H[m - off][m])),
 // zero where row m does not cross the global diagonal (off = r0 - c0)
-__global__ void oz_diag(const double2* H, int64_t ld, int p, int q, int dir, int off, double2* d) {
+__device__ __forceinline__ double2 as_c(double2 v) { return v; }
+__device__ __forceinline__ double2 as_c(double v) { return make_double2(v, 0.0); }
+template <class T>
+__global__ void oz_diag(const T* H, int64_t ld, int p, int q, int dir, int off, double2* d) {
   const int m = blockIdx.x * 256 + threadIdx.x;
   const int lines = dir == 0 ? p : q;
   if (m >= lines) return;
   double2 v = make_double2(0.0, 0.0);
   if (dir == 0) {
     const int j = m + off;
-    if (j >= 0 && j < q) v = H[m + (int64_t)j * ld];
+    if (j >= 0 && j < q) v = as_c(H[m + (int64_t)j * ld]);
   } else {
     const int i = m - off;
-    if (i >= 0 && i < p) { v = H[i + (int64_t)m * ld]; v.y = -v.y; }
+    if (i >= 0 && i < p) { v = as_c(H[i + (int64_t)m * ld]); v.y = -v.y; }
   }
   d[m] = v;
 }
@@ -539,22 +575,22 @@ using OzShard = chase_handle::OzShard;    // slices of the shard for one directi
 
 static int oz_slices_opt(chase_handle* h) { return std::min(8, std::max(0, h->opt.fp64_emulation)); }
 
-template <int S>
-static void slice_lines(const double2* X, int64_t ld, int rows, int lines, bool conj, int diag, int8_t* out,
-                        int64_t ldk, int64_t plane, int* e, cudaStream_t st) {
+template <int S, class T>
+static void slice_lines(const T* X, int64_t ld, int rows, int lines, bool conj, int diag, int8_t* out, int64_t ldk,
+                        int64_t plane, int* e, cudaStream_t st) {
   if (lines <= 0) return;
-  oz::oz_slice_lines<S><<<lines, 256, 0, st>>>(X, ld, rows, lines, conj ? 1 : 0, diag, out, ldk, plane, e);
+  oz::oz_slice_lines<S, T><<<lines, 256, 0, st>>>(X, ld, rows, lines, conj ? 1 : 0, diag, out, ldk, plane, e);
   CHASE_CHECK_LAUNCH();
 }
 
-template <int S>
-static void slice_rows(const double2* H, int64_t ld, int rows, int cols, int diag, unsigned long long* mx,
-                       int8_t* out, int64_t ldk, int64_t plane, int* e, cudaStream_t st) {
-  CHASE_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * 3 * rows, st));
-  oz::oz_row_max<<<dim3(ceil_div(rows, 256), ceil_div(cols, 256)), 256, 0, st>>>(H, ld, rows, cols, diag, mx);
+template <int S, class T>
+static void slice_rows(const T* H, int64_t ld, int rows, int cols, int diag, unsigned long long* mx, int8_t* out,
+                       int64_t ldk, int64_t plane, int* e, cudaStream_t st) {
+  CHASE_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * oz::Comp<T>::NP * rows, st));
+  oz::oz_row_max<T><<<dim3(ceil_div(rows, 256), ceil_div(cols, 256)), 256, 0, st>>>(H, ld, rows, cols, diag, mx);
   CHASE_CHECK_LAUNCH();
-  oz::oz_slice_rows<S><<<dim3(ceil_div(rows, 32), ceil_div(ldk, 64)), 256, 0, st>>>(H, ld, rows, cols, diag, mx, out,
-                                                                                    ldk, plane, e);
+  oz::oz_slice_rows<S, T><<<dim3(ceil_div(rows, 32), ceil_div(ldk, 64)), 256, 0, st>>>(H, ld, rows, cols, diag, mx,
+                                                                                       out, ldk, plane, e);
   CHASE_CHECK_LAUNCH();
 }
 
@@ -571,33 +607,36 @@ static void with_S(int S, F&& f) {
   }
 }
 
-// the A operand of direction dir for this shard: slices [3 S][lines][ldk] + exponents [3][lines]
+// the A operand of direction dir for this shard: slices [NP S][lines][ldk] + exponents [NP][lines]
+// + the diagonal of the split
+template <class T>
 static const OzShard& oz_shard(chase_handle* h, int dir, const void* H, int64_t ldh) {
+  constexpr int NP = oz::Comp<T>::NP;
   OzShard& z = dir == 0 ? h->oz_fwd : h->oz_bwd;
   const int S = oz_slices_opt(h);
   if (z.src == H && z.ld == ldh && z.S == S && z.slices.p) return z;
   const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
   const int lines = dir == 0 ? (int)p : (int)q, K = dir == 0 ? (int)q : (int)p;
   const int64_t ldk = oz::ldk_of(K);
-  z.slices.alloc((size_t)3 * S * lines * ldk);
-  z.exps.alloc(sizeof(int) * 3 * (size_t)lines + sizeof(unsigned long long) * 3 * (size_t)lines + 16);
+  z.slices.alloc((size_t)NP * S * lines * ldk);
+  z.exps.alloc(sizeof(int) * NP * (size_t)lines + sizeof(unsigned long long) * NP * (size_t)lines + 16);
   int* e = z.exps.as<int>();
-  unsigned long long* mx = reinterpret_cast<unsigned long long*>(e + 3 * (size_t)lines + (3 * lines & 1));
-  const double2* Hz = reinterpret_cast<const double2*>(H);
+  unsigned long long* mx = reinterpret_cast<unsigned long long*>(e + NP * (size_t)lines + (NP * lines & 1));
+  const T* Hz = reinterpret_cast<const T*>(H);
   // diagonal split: global diagonal of H in local coordinates (row i, column i + (r0 - c0))
   const int64_t r0 = h->grid.rows.start, c0 = h->grid.cols.start;
   with_S(S, [&](auto Sc) {
     constexpr int SS = decltype(Sc)::value;
     if (dir == 0)
-      slice_rows<SS>(Hz, ldh, (int)p, (int)q, (int)(r0 - c0), mx, z.slices.as<int8_t>(), ldk, (int64_t)lines * ldk, e,
-                     h->stream);
+      slice_rows<SS, T>(Hz, ldh, (int)p, (int)q, (int)(r0 - c0), mx, z.slices.as<int8_t>(), ldk, (int64_t)lines * ldk,
+                        e, h->stream);
     else   // A = H^H: line j = column j of H, conjugated; its diagonal element is row j + (c0 - r0)
-      slice_lines<SS>(Hz, ldh, (int)p, (int)q, true, (int)(c0 - r0), z.slices.as<int8_t>(), ldk, (int64_t)lines * ldk,
-                      e, h->stream);
+      slice_lines<SS, T>(Hz, ldh, (int)p, (int)q, true, (int)(c0 - r0), z.slices.as<int8_t>(), ldk,
+                         (int64_t)lines * ldk, e, h->stream);
   });
   z.diag.alloc(sizeof(double2) * (size_t)lines);
-  oz::oz_diag<<<ceil_div(lines, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, dir, (int)(r0 - c0),
-                                                          z.diag.as<double2>());
+  oz::oz_diag<T><<<ceil_div(lines, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, dir, (int)(r0 - c0),
+                                                             z.diag.as<double2>());
   CHASE_CHECK_LAUNCH();
   z.src = H;
   z.ld = ldh;
@@ -605,26 +644,29 @@ static const OzShard& oz_shard(chase_handle* h, int dir, const void* H, int64_t 
   return z;
 }
 
-// Y = alpha (op(H) X - gamma E X) + beta Y  (one rank's local part of a fused step, complex double)
-void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
+// Y = alpha (op(H) X - gamma E X) + beta Y  (one rank's local part of a fused step; T = double2
+// complex Hermitian, T = double real symmetric)
+template <class T>
+static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
+  constexpr int NP = oz::Comp<T>::NP;
   const int S = oz_slices_opt(h);
   const int dir = d.conjA ? 1 : 0;
-  const OzShard& A = oz_shard(h, dir, d.A, d.lda);
+  const OzShard& A = oz_shard<T>(h, dir, d.A, d.lda);
   const int M = d.M, N = d.N, K = d.K;
   if (M <= 0 || N <= 0) return;
   cudaStream_t st = h->stream;
   // B operand: the block X (columns contiguous in k)
   const int64_t ldkb = oz::ldk_of(K);
-  h->oz_b.alloc((size_t)3 * S * N * ldkb + sizeof(int) * 3 * (size_t)N + 64);
+  h->oz_b.alloc((size_t)NP * S * N * ldkb + sizeof(int) * NP * (size_t)N + 64);
   int8_t* bsl = h->oz_b.as<int8_t>();
-  int* fB = reinterpret_cast<int*>(bsl + (size_t)3 * S * N * ldkb);
+  int* fB = reinterpret_cast<int*>(bsl + (size_t)NP * S * N * ldkb);
   with_S(S, [&](auto Sc) {
-    slice_lines<decltype(Sc)::value>(reinterpret_cast<const double2*>(d.B), d.ldb, K, N, false, INT_MIN, bsl, ldkb,
-                                     (int64_t)N * ldkb, fB, st);
+    slice_lines<decltype(Sc)::value, T>(reinterpret_cast<const T*>(d.B), d.ldb, K, N, false, INT_MIN, bsl, ldkb,
+                                        (int64_t)N * ldkb, fB, st);
   });
-  // FP64 accumulators of the three real products
-  h->oz_t.alloc(sizeof(double) * 3 * (size_t)M * N);
-  double* T = h->oz_t.as<double>();
+  // FP64 accumulators of the real products
+  h->oz_t.alloc(sizeof(double) * NP * (size_t)M * N);
+  double* Tacc = h->oz_t.as<double>();
   static unsigned long long attr = 0;
   if (first_on_device(attr))
     CHASE_CUDA(cudaFuncSetAttribute(oz::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
@@ -646,7 +688,7 @@ void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
     CHASE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const int grid = 2 * std::min(ptiles, sms / 2);            // persistent: one CTA pair per 2 SMs
-  for (int P = 0; P < 3; ++P) {
+  for (int P = 0; P < NP; ++P) {
     CUtensorMap ta, tb;
     oz::make_slice_tmap(&ta, A.slices.as<int8_t>() + (size_t)P * S * lines_a * ldka, K, lines_a, ldka, S, oz::BM);
     oz::make_slice_tmap(&tb, bsl + (size_t)P * S * N * ldkb, K, N, ldkb, S, oz::BN / 2);
@@ -664,7 +706,7 @@ void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
           prm.tb[q] = pairs[b0 + q].second;
         }
         prm.scale = std::ldexp(1.0, -7 * dsum);
-        prm.out = T + (size_t)P * M * N;
+        prm.out = Tacc + (size_t)P * M * N;
         prm.ldo = M;
         prm.accumulate = first ? 0 : 1;
         prm.hint = hint_env;
@@ -690,11 +732,15 @@ void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
   } else {
     dlo = (int)std::max<int64_t>(0, r0 - c0); dhi = (int)std::min<int64_t>(q, r0 + p - c0); doff = c0 - r0;
   }
-  oz::oz_combine<<<148 * 8, 256, 0, st>>>(T, M, (int64_t)M * N, eA, M, fB, N, reinterpret_cast<double2*>(d.C), d.ldc,
-                                          d.alpha, d.beta, d.beta != 0.0 ? 1 : 0,
-                                          reinterpret_cast<const double2*>(d.B), d.ldb, A.diag.as<double2>(), dlo,
-                                          std::max(dlo, dhi), doff, d.gamma);
+  oz::oz_combine<T><<<148 * 8, 256, 0, st>>>(Tacc, M, (int64_t)M * N, eA, M, fB, N, reinterpret_cast<T*>(d.C), d.ldc,
+                                             d.alpha, d.beta, d.beta != 0.0 ? 1 : 0, reinterpret_cast<const T*>(d.B),
+                                             d.ldb, A.diag.as<double2>(), dlo, std::max(dlo, dhi), doff, d.gamma);
   CHASE_CHECK_LAUNCH();
+}
+
+void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
+  if (h->real()) ozaki_step_t<double>(h, d);
+  else ozaki_step_t<double2>(h, d);
 }
 
 void ozaki_release(chase_handle* h) {

@@ -118,3 +118,40 @@ def test_shard_rewritten_in_place_is_resliced(dtype):
         ch.hemm_step(0, dH, dX, dY, n, 1.0, 0.0, 0.0)
         ref = H.astype(complex) @ X.astype(complex)
         assert _rel(dY.cpu().numpy().astype(complex), ref) <= tol
+
+
+@pytest.mark.parametrize("direction", [0, 1])
+def test_real_emulated_product_exact_and_step_vs_oracle(direction):
+    """Real-symmetric variant (f2): one real product per step (no 3M)."""
+    import paper_2205_02491_b200 as pkg
+    N, n = 700, 45
+    rng = np.random.default_rng(3)
+    Hi = rng.integers(-100, 101, (N, N))
+    Xi = rng.integers(-50, 51, (N, n))
+    ref = ((Hi if direction == 0 else Hi.T) @ Xi) * 2.0 ** -13
+    ch = pkg.Chase(N, n, 1, dtype="r64")
+    ch.set_option("fp64_emulation", 7)
+    dY = _dev(np.zeros((N, n)))
+    ch.hemm_step(direction, _dev(Hi * 2.0 ** -10), _dev(Xi * 2.0 ** -3), dY, n, 1.0, 0.0, 0.0)
+    assert np.array_equal(dY.cpu().numpy(), ref)
+    M = make_matrix("uniform", N, "r2", seed=4)
+    H = M.dense()
+    X, Y0 = rng.standard_normal((N, n)), rng.standard_normal((N, n))
+    ref = oracle.hemm_step(H, X, Y0, 0.37, -0.81, 0.55)
+    dY = _dev(Y0)
+    ch.hemm_step(direction, _dev(H), _dev(X), dY, n, 0.37, -0.81, 0.55)
+    assert _rel(dY.cpu().numpy(), ref) <= 1e-13
+
+
+def test_real_emulated_solve():
+    import paper_2205_02491_b200 as pkg
+    N, nev, nex = 800, 40, 20
+    M = make_matrix("wilkinson", N, "r2", seed=7)
+    H = M.dense()
+    ch = pkg.Chase(N, nev, nex, dtype="r64")
+    vals, vecs, rep, st = ch.solve(_dev(H), nev, nex, deg=20, tol=1e-10)
+    assert st == 0
+    normH = np.max(np.abs(M.lam))
+    assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
+    V = vecs.cpu().numpy()[:, :nev]
+    assert np.max(np.linalg.norm(H @ V - V * vals[None, :], axis=0)) <= 1e-10 * normH

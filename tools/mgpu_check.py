@@ -48,7 +48,7 @@ def main():
     assert ch.local_layout() == (r0, p, c0, q)
     if os.environ.get("MG_FUSED_C64"):
         ch.set_option("fused_reduce_c64", 1)
-    if not single and not real:
+    if not single:
         ch.set_option("fp64_emulation", int(os.environ.get("MG_OZAKI", "0")))   # 0: DMMA + fused f1 epilogue
     dH = dev(cast(H[r0:r0 + p, c0:c0 + q]))
     ok = True
