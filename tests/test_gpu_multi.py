@@ -17,13 +17,15 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("dtype", ["c128", "c64", "c64-fused", "r64"])
+@pytest.mark.parametrize("dtype", ["c128", "c128-ozaki", "c64", "c64-fused", "r64", "r64-ozaki"])
 def test_two_gpu_grid(dtype):
     if _ngpu() < 2:
         pytest.skip("needs >= 2 GPUs")
     env = dict(os.environ, MG_DTYPE=dtype.split("-")[0], CHASE_DEBUG_PEER="1")
     if dtype == "c64-fused":
         env["MG_FUSED_C64"] = "1"
+    if dtype.endswith("-ozaki"):
+        env["MG_OZAKI"] = "7"          # Ozaki INT8 emulation of the FP64 products + NCCL all-reduce
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "tools", "mgpu_check.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
