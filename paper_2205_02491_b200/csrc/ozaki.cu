@@ -398,22 +398,36 @@ __global__ void __launch_bounds__(256) oz_slice_lines(const T* X, int64_t ld, in
   double sc[NP];
 #pragma unroll
   for (int P = 0; P < NP; ++P) sc[P] = ldexp(1.0, -ex[P]);
-  for (int k = threadIdx.x; k < (int)ldk; k += 256) {
-    int8_t a[NP][S];
-    double v[NP];
-    if (k < rows && k != kd) {
-      Comp<T>::get(x[k], sg, v);
-    } else {
-#pragma unroll
-      for (int P = 0; P < NP; ++P) v[P] = 0.0;
-    }
-#pragma unroll
-    for (int P = 0; P < NP; ++P) cut<S>(v[P] * sc[P], a[P]);
-    int8_t* o = out + (int64_t)c * ldk + k;
+  // 4 consecutive k per thread: one 4-byte store per slice (ldk % 128 == 0)
+  for (int k4 = threadIdx.x * 4; k4 < (int)ldk; k4 += 256 * 4) {
+    uint32_t packed[NP][S];
 #pragma unroll
     for (int P = 0; P < NP; ++P)
 #pragma unroll
-      for (int s = 0; s < S; ++s) o[(int64_t)(P * S + s) * plane] = a[P][s];
+      for (int s = 0; s < S; ++s) packed[P][s] = 0;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k4 + kk;
+      double v[NP];
+      if (k < rows && k != kd) {
+        Comp<T>::get(x[k], sg, v);
+      } else {
+#pragma unroll
+        for (int P = 0; P < NP; ++P) v[P] = 0.0;
+      }
+      int8_t a[NP][S];
+#pragma unroll
+      for (int P = 0; P < NP; ++P) cut<S>(v[P] * sc[P], a[P]);
+#pragma unroll
+      for (int P = 0; P < NP; ++P)
+#pragma unroll
+        for (int s = 0; s < S; ++s) packed[P][s] |= (uint32_t)(uint8_t)a[P][s] << (8 * kk);
+    }
+    int8_t* o = out + (int64_t)c * ldk + k4;
+#pragma unroll
+    for (int P = 0; P < NP; ++P)
+#pragma unroll
+      for (int s = 0; s < S; ++s) *reinterpret_cast<uint32_t*>(o + (int64_t)(P * S + s) * plane) = packed[P][s];
   }
 }
 
@@ -469,21 +483,31 @@ __global__ void __launch_bounds__(256) oz_slice_rows(const T* H, int64_t ld, int
 #pragma unroll
     for (int P = 0; P < NP; ++P) e[P * rows + i] = ex[P];
   }
-#pragma unroll 1
+  // 8 consecutive k of row i per thread: one 8-byte store per slice (ldk % 128 == 0, j % 8 == 0)
+  const int jb = j0 + jg;
+  if (jb >= (int)ldk) return;
+  uint64_t packed[NP][S];
+#pragma unroll
+  for (int P = 0; P < NP; ++P)
+#pragma unroll
+    for (int s = 0; s < S; ++s) packed[P][s] = 0;
+#pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
-    const int j = j0 + jg + jj;
-    if (j >= (int)ldk) break;
     double v[NP];
     Comp<T>::get(t[jg + jj][ii], 1.0, v);
     int8_t a[NP][S];
 #pragma unroll
     for (int P = 0; P < NP; ++P) cut<S>(v[P] * sc[P], a[P]);
-    int8_t* o = out + (int64_t)i * ldk + j;
 #pragma unroll
     for (int P = 0; P < NP; ++P)
 #pragma unroll
-      for (int s = 0; s < S; ++s) o[(int64_t)(P * S + s) * plane] = a[P][s];
+      for (int s = 0; s < S; ++s) packed[P][s] |= (uint64_t)(uint8_t)a[P][s] << (8 * jj);
   }
+  int8_t* o = out + (int64_t)i * ldk + jb;
+#pragma unroll
+  for (int P = 0; P < NP; ++P)
+#pragma unroll
+    for (int s = 0; s < S; ++s) *reinterpret_cast<uint64_t*>(o + (int64_t)(P * S + s) * plane) = packed[P][s];
 }
 
 // Y = alpha (C - gamma E X) + beta Y from the FP64 real products with their exponents (complex:
@@ -672,8 +696,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
     CHASE_CUDA(cudaFuncSetAttribute(oz::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
   const int lines_a = M;
   const int64_t ldka = oz::ldk_of(K);
-  // pairs per int32 accumulator: npairs 127^2 K <= 2^31 - 1 (exact accumulation)
-  int cap = (int)std::max<int64_t>(1, std::min<int64_t>(oz::MAX_PAIRS, 2147483647LL / (16129LL * K)));
+  int cap = oz::MAX_PAIRS;                                  // pairs per launch (see the packing below)
   static const int cap_env = [] { const char* e = std::getenv("CHASE_OZ_PAIRS"); return e ? std::atoi(e) : 0; }();
   if (cap_env > 0) cap = std::min(cap, cap_env);          // tuning knob: slice pairs per launch
   static const int hint_env = [] { const char* e = std::getenv("CHASE_OZ_HINT"); return e ? std::atoi(e) : 0; }();
@@ -697,10 +720,21 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
       std::vector<std::pair<int, int>> pairs;
       for (int s = 1; s < dsum; ++s)
         if (s <= S && dsum - s <= S) pairs.push_back({s - 1, dsum - s - 1});
-      for (size_t b0 = 0; b0 < pairs.size(); b0 += cap) {
+      // pack the group's pairs into launches whose int32 sums stay exact: |a_1| <= 127 and
+      // |a_s| <= 64 (s >= 2, round-to-nearest slices), so a pair contributes at most
+      // m_s m_t K per output and a launch may hold pairs while sum m_s m_t K <= 2^31 - 1
+      // (at K = 30000 every d group fits one launch: 7 launches per real product)
+      auto mag = [](int s0) { return s0 == 0 ? 127LL : 64LL; };
+      for (size_t b0 = 0, b1; b0 < pairs.size(); b0 = b1) {
+        long long bound = 0;
+        for (b1 = b0; b1 < pairs.size() && (int)(b1 - b0) < cap; ++b1) {
+          const long long add = mag(pairs[b1].first) * mag(pairs[b1].second) * (long long)K;
+          if (b1 > b0 && bound + add > 2147483647LL) break;
+          bound += add;
+        }
         oz::Params prm{};
         prm.M = M; prm.N = N; prm.K = K;
-        prm.npairs = (int)std::min<size_t>(cap, pairs.size() - b0);
+        prm.npairs = (int)(b1 - b0);
         for (int q = 0; q < prm.npairs; ++q) {
           prm.sa[q] = pairs[b0 + q].first;
           prm.tb[q] = pairs[b0 + q].second;
