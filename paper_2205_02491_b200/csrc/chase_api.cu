@@ -380,7 +380,6 @@ chase_status guarded(chase_handle* h, F&& f, bool collective = true) {
 // address back for a different matrix, between calls.
 void invalidate_shard_caches(chase_handle* h) {
   h->oz_fwd.src = nullptr;
-  h->oz_bwd.src = nullptr;
   h->hlo_src = nullptr;
   h->h32_src = nullptr;
 }

@@ -105,12 +105,12 @@ struct chase_handle {
   chase::DBuf c64v, c64w;              // c64: planar V-layout / W-layout operand formats (c64.cu)
   chase::DBuf H32;                     // f4: complex-single shadow of a complex-double shard
   chase::DBuf Hstage, Vstage;          // chase_solve with host buffers: device copies of H / vectors
-  struct OzShard {                     // fp64_emulation: int8 slices of the shard per direction (ozaki.cu)
+  struct OzShard {                     // fp64_emulation: the shard's int8 slice set (ozaki.cu)
     const void* src = nullptr;
     int64_t ld = 0;
     int S = 0;
     chase::DBuf slices, exps, diag;
-  } oz_fwd, oz_bwd;
+  } oz_fwd;
   bool oz_off = false;                 // fp64_emulation fell back to DMMA (slices did not fit)
   chase::DBuf oz_b, oz_t, oz_sync;     // fp64_emulation: slices of the block X, FP64 product accumulators
   const void* h32_src = nullptr;

@@ -14,10 +14,12 @@
 // exact).  With S = 7 the truncation error is ~2^-49 |X||Y| per entry, below the FP64 step bar
 // of 1e-13 by two orders of magnitude.
 //
-// Data.  The H shard's slices are built once per shard (and direction): forward A = H (rows of H
-// contiguous in k: a transposing slicer), backward A = H^H (columns of H contiguous in k; the
-// imaginary part negated).  Every step slices the block X (columns contiguous in k).  All slice
-// matrices are K-major int8 [slice][row][ldk], TMA-loaded as 128-byte swizzled rows.
+// Data.  The H shard is equilibrated (H_P = D_r Hhat_P D_c, power-of-two row and column scalings,
+// diagonal excluded) and Hhat_P sliced ONCE per API call into int8 [slice][j][i] (columns of H,
+// i contiguous): the backward step (A = H^H) reads it as a K-major operand, the forward step
+// (A = H) as an MN-major one (tcgen05 transpose bit), and the scalings fold into the B operand
+// (D_c X forward, D_r W backward) and the output rows.  Every step slices its block X (columns
+// contiguous in k), TMA-loaded as 128-byte swizzled rows.
 //
 // Kernel (oz_gemm_kernel): persistent CTA pairs (tcgen05 cta_group::2), 256 x 256 output tiles,
 // 192 threads per CTA: warp 0 TMA producer into a 6-stage ring (16 KB of A rows + 16 KB of B
@@ -60,9 +62,22 @@ struct Params {
   int accumulate;                      // 0: out = scale acc; 1: out += scale acc
   int hint;                            // 1: L2 evict_first for A (streamed), evict_last for B (re-read)
   unsigned* sync;                      // round barrier counter (zeroed per launch); null = no barrier
+  int amn;                             // 1: A is MN-major (slices [k][m], m contiguous: the forward step)
 };
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {   // K-major, SWIZZLE_128B, 8-row groups 1 KB apart
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// MN-major A (int8, SWIZZLE_128B): one 128-byte m atom (the CTA's 128 rows) per k row, 8-row
+// groups 1 KB apart; one MMA (K = 32) spans 32 k rows = 4 KB (validated by
+// tools/microbench/i8_mn_probe.cu: bit-exact against the CPU product)
+__device__ __forceinline__ uint64_t sdesc_mn(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)(16 >> 4) << 16;
@@ -216,11 +231,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const uint32_t st = smem_u32(sm + s * STAGE_BYTES);
             const uint32_t fb = mapa0(smem_u32(full + s));
             if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * STAGE_BYTES);
+            // A box {128, 128, 1}: K-major coordinates (k, m), MN-major (m, k)
+            const int ac0 = p.amn ? m0 : kt * BK, ac1 = p.amn ? kt * BK : m0;
             if (p.hint) {
-              tma_3d_pair_hint(st, &tA, kt * BK, m0, p.sa[q], fb, pol_a);
+              tma_3d_pair_hint(st, &tA, ac0, ac1, p.sa[q], fb, pol_a);
               tma_3d_pair_hint(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb, pol_b);
             } else {
-              tma_3d_pair(st, &tA, kt * BK, m0, p.sa[q], fb);
+              tma_3d_pair(st, &tA, ac0, ac1, p.sa[q], fb);
               tma_3d_pair(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb);
             }
           }
@@ -232,8 +249,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t leader;
       asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
       // S32 accumulate, signed int8 A and B, both K-major, N = 256, M = 256 (pair)
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)((2 * BM) >> 4) << 24);
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((p.amn ? 1u : 0u) << 15) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
       int it = 0, tl = 0;
       for (int r = 0; r < NT; ++r, ++tl) {
         const int b = tl & 1;
@@ -253,7 +270,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
               asm volatile(
                   "{ .reg .pred q; setp.ne.b32 q, %4, 0; tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, q; }"
-                  ::"r"(td), "l"(sdesc(sa + kk * 32)), "l"(sdesc(sb + kk * 32)), "r"(idesc), "r"(acc));
+                  ::"r"(td), "l"(p.amn ? sdesc_mn(sa + kk * 4096) : sdesc(sa + kk * 32)), "l"(sdesc(sb + kk * 32)),
+                    "r"(idesc), "r"(acc));
             }
             commit_both(empty + s);
           }
@@ -335,16 +353,15 @@ __device__ __forceinline__ void cut(double v, int8_t (&a)[S]) {
   }
 }
 
-// The NP real matrices the products run on: complex (NP = 3, Gauss's 3M): re, im (negated if
-// conj), re + im; real symmetric (NP = 1): the value itself.
+// The NP real matrices the products run on: complex (NP = 3, Gauss's 3M): re, im, re + sg im
+// (sg = -1 for the B operand of the backward step, see ozaki_step_t); real symmetric (NP = 1).
 template <class T> struct Comp;
 template <> struct Comp<double2> {
   static constexpr int NP = 3;
   __device__ static void get(double2 v, double sg, double (&c)[3]) {
-    const double im = sg * v.y;
     c[0] = v.x;
-    c[1] = im;
-    c[2] = v.x + im;
+    c[1] = v.y;
+    c[2] = v.x + sg * v.y;
   }
   __device__ static double2 zero() { return make_double2(0.0, 0.0); }
 };
@@ -355,27 +372,36 @@ template <> struct Comp<double> {
 };
 
 // Lines contiguous in memory (columns of a column-major matrix): line c of `rows` values at
-// X + c ld.  Writes, for every real component P (Comp), slices out[(P S + s) * plane + c * ldk + k]
-// and exponents e[P * lines + c].  One CTA per line.
+// X + c ld, each value k first scaled by 2^(ksg kexp[P kexp_ld + k]) if kexp is given (the
+// equilibration of the shard, see ozaki_step_t).  Writes, for every real component P (Comp),
+// slices out[(P S + s) * plane + c * ldk + k] and exponents e[P * lines + c].  One CTA per line.
 // diag != INT_MIN: the element k = c + diag of line c lies on the global diagonal of H; it is left
 // out of the slices (zero) and added exactly in FP64 by oz_combine (diagonal split: the dominant
 // diagonal of a Hermitian H would otherwise set the line's exponent and cost the off-diagonal
 // entries their low bits).
 template <int S, class T>
-__global__ void __launch_bounds__(256) oz_slice_lines(const T* X, int64_t ld, int rows, int lines, int conj,
-                                                      int diag, int8_t* out, int64_t ldk, int64_t plane, int* e) {
+__global__ void __launch_bounds__(256) oz_slice_lines(const T* X, int64_t ld, int rows, int lines, int sg3,
+                                                      int diag, const int* kexp, int kexp_ld, int ksg, int8_t* out,
+                                                      int64_t ldk, int64_t plane, int* e) {
   constexpr int NP = Comp<T>::NP;
   const int c = blockIdx.x;
   const T* x = X + (int64_t)c * ld;
-  const double sg = conj ? -1.0 : 1.0;
+  const double sg = sg3 < 0 ? -1.0 : 1.0;
   const int kd = diag == INT_MIN ? -1 : c + diag;
+  auto load = [&](int k, double (&v)[NP]) {
+    Comp<T>::get(x[k], sg, v);
+    if (kexp) {
+#pragma unroll
+      for (int P = 0; P < NP; ++P) v[P] = ldexp(v[P], ksg * kexp[P * kexp_ld + k]);
+    }
+  };
   double mx[NP];
 #pragma unroll
   for (int P = 0; P < NP; ++P) mx[P] = 0.0;
   for (int k = threadIdx.x; k < rows; k += 256) {
     if (k == kd) continue;
     double v[NP];
-    Comp<T>::get(x[k], sg, v);
+    load(k, v);
 #pragma unroll
     for (int P = 0; P < NP; ++P) mx[P] = fmax(mx[P], fabs(v[P]));
   }
@@ -410,7 +436,7 @@ __global__ void __launch_bounds__(256) oz_slice_lines(const T* X, int64_t ld, in
       const int k = k4 + kk;
       double v[NP];
       if (k < rows && k != kd) {
-        Comp<T>::get(x[k], sg, v);
+        load(k, v);
       } else {
 #pragma unroll
         for (int P = 0; P < NP; ++P) v[P] = 0.0;
@@ -453,61 +479,13 @@ __global__ void oz_row_max(const T* H, int64_t ld, int rows, int cols, int diag,
   for (int P = 0; P < NP; ++P) atomicMax(mx + P * rows + i, (unsigned long long)__double_as_longlong(m[P]));
 }
 
-// Transposing slicer for the forward A operand: row i of H (strided) -> line i of the output
-// (contiguous in k = column index j).  Tile of 32 rows x 64 columns through shared memory.
-template <int S, class T>
-__global__ void __launch_bounds__(256) oz_slice_rows(const T* H, int64_t ld, int rows, int cols, int diag,
-                                                     const unsigned long long* mx, int8_t* out, int64_t ldk,
-                                                     int64_t plane, int* e) {
-  constexpr int NP = Comp<T>::NP;
-  __shared__ T t[64][33];
-  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 64;
-  for (int idx = threadIdx.x; idx < 32 * 64; idx += 256) {
-    const int ii = idx & 31, jj = idx >> 5;
-    const int i = i0 + ii, j = j0 + jj;
-    t[jj][ii] = (i < rows && j < cols && j != i + diag) ? H[i + (int64_t)j * ld] : Comp<T>::zero();
-  }
-  __syncthreads();
-  // thread -> (row ii, 8-column group): 8 consecutive k per slice
-  const int ii = threadIdx.x >> 3, jg = (threadIdx.x & 7) * 8;
-  const int i = i0 + ii;
+// row exponents of the equilibration: r[P][i] from the row maxima (line_exp)
+template <class T>
+__global__ void oz_row_exp(const unsigned long long* mx, int rows, int* r) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= rows) return;
-  int ex[NP];
-  double sc[NP];
 #pragma unroll
-  for (int P = 0; P < NP; ++P) {
-    ex[P] = line_exp(__longlong_as_double((long long)mx[P * rows + i]));
-    sc[P] = ldexp(1.0, -ex[P]);
-  }
-  if (blockIdx.y == 0 && (threadIdx.x & 7) == 0) {
-#pragma unroll
-    for (int P = 0; P < NP; ++P) e[P * rows + i] = ex[P];
-  }
-  // 8 consecutive k of row i per thread: one 8-byte store per slice (ldk % 128 == 0, j % 8 == 0)
-  const int jb = j0 + jg;
-  if (jb >= (int)ldk) return;
-  uint64_t packed[NP][S];
-#pragma unroll
-  for (int P = 0; P < NP; ++P)
-#pragma unroll
-    for (int s = 0; s < S; ++s) packed[P][s] = 0;
-#pragma unroll
-  for (int jj = 0; jj < 8; ++jj) {
-    double v[NP];
-    Comp<T>::get(t[jg + jj][ii], 1.0, v);
-    int8_t a[NP][S];
-#pragma unroll
-    for (int P = 0; P < NP; ++P) cut<S>(v[P] * sc[P], a[P]);
-#pragma unroll
-    for (int P = 0; P < NP; ++P)
-#pragma unroll
-      for (int s = 0; s < S; ++s) packed[P][s] |= (uint64_t)(uint8_t)a[P][s] << (8 * jj);
-  }
-  int8_t* o = out + (int64_t)i * ldk + jb;
-#pragma unroll
-  for (int P = 0; P < NP; ++P)
-#pragma unroll
-    for (int s = 0; s < S; ++s) *reinterpret_cast<uint64_t*>(o + (int64_t)(P * S + s) * plane) = packed[P][s];
+  for (int P = 0; P < Comp<T>::NP; ++P) r[P * rows + i] = line_exp(__longlong_as_double((long long)mx[P * rows + i]));
 }
 
 // Y = alpha (C - gamma E X) + beta Y from the FP64 real products with their exponents (complex:
@@ -519,7 +497,7 @@ __device__ __forceinline__ double2 c_fma(double a, double2 v, double2 acc) {
 template <class T>
 __global__ void oz_combine(const double* T_, int64_t ldt, int64_t tplane, const int* eA, int M, const int* fB, int N,
                            T* Y, int64_t ldy, double alpha, double beta, int beta_on, const T* X, int64_t ldx,
-                           const double2* hdiag, int dlo, int dhi, int64_t doff, double gamma) {
+                           const double2* hdiag, int dlo, int dhi, int64_t doff, double gamma, int dir) {
   const int64_t total = (int64_t)M * N;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int m = (int)(idx % M), n = (int)(idx / M);
@@ -529,7 +507,11 @@ __global__ void oz_combine(const double* T_, int64_t ldt, int64_t tplane, const 
     if constexpr (Comp<T>::NP == 3) {
       const double t2 = ldexp(T_[tplane + o], eA[M + m] + fB[N + n]);
       const double t3 = ldexp(T_[2 * tplane + o], eA[2 * M + m] + fB[2 * N + n]);
-      double re = alpha * (t1 - t2), im = alpha * (t3 - t1 - t2);
+      // forward (H X): Re = T1 - T2, Im = T3 - T1 - T2 with T3 = (Hr + Hi)(Xr + Xi);
+      // backward (H^H W): Re = T1 + T2, Im = T1 - T2 - T3 with T3 = (Hr + Hi)(Wr - Wi)
+      double re, im;
+      if (dir == 0) { re = alpha * (t1 - t2); im = alpha * (t3 - t1 - t2); }
+      else { re = alpha * (t1 + t2); im = alpha * (t1 - t2 - t3); }
       if (m >= dlo && m < dhi) {
         const double2 x = X[(int64_t)m + doff + (int64_t)n * ldx];
         const double2 hd = hdiag[m];
@@ -595,26 +577,16 @@ inline int64_t ldk_of(int64_t K) { return (K + 127) / 128 * 128; }   // 16-B TMA
 }  // namespace oz
 
 // ------------------------------------------------------------------------------------ host
-using OzShard = chase_handle::OzShard;    // slices of the shard for one direction (cached on the handle)
+using OzShard = chase_handle::OzShard;    // the shard's slice set (cached on the handle within one API call)
 
 static int oz_slices_opt(chase_handle* h) { return std::min(8, std::max(0, h->opt.fp64_emulation)); }
 
 template <int S, class T>
-static void slice_lines(const T* X, int64_t ld, int rows, int lines, bool conj, int diag, int8_t* out, int64_t ldk,
-                        int64_t plane, int* e, cudaStream_t st) {
+static void slice_lines(const T* X, int64_t ld, int rows, int lines, int sg3, int diag, const int* kexp, int kexp_ld,
+                        int ksg, int8_t* out, int64_t ldk, int64_t plane, int* e, cudaStream_t st) {
   if (lines <= 0) return;
-  oz::oz_slice_lines<S, T><<<lines, 256, 0, st>>>(X, ld, rows, lines, conj ? 1 : 0, diag, out, ldk, plane, e);
-  CHASE_CHECK_LAUNCH();
-}
-
-template <int S, class T>
-static void slice_rows(const T* H, int64_t ld, int rows, int cols, int diag, unsigned long long* mx, int8_t* out,
-                       int64_t ldk, int64_t plane, int* e, cudaStream_t st) {
-  CHASE_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * oz::Comp<T>::NP * rows, st));
-  oz::oz_row_max<T><<<dim3(ceil_div(rows, 256), ceil_div(cols, 256)), 256, 0, st>>>(H, ld, rows, cols, diag, mx);
-  CHASE_CHECK_LAUNCH();
-  oz::oz_slice_rows<S, T><<<dim3(ceil_div(rows, 32), ceil_div(ldk, 64)), 256, 0, st>>>(H, ld, rows, cols, diag, mx,
-                                                                                       out, ldk, plane, e);
+  oz::oz_slice_lines<S, T><<<lines, 256, 0, st>>>(X, ld, rows, lines, sg3, diag, kexp, kexp_ld, ksg, out, ldk, plane,
+                                                  e);
   CHASE_CHECK_LAUNCH();
 }
 
@@ -631,36 +603,48 @@ static void with_S(int S, F&& f) {
   }
 }
 
-// the A operand of direction dir for this shard: slices [NP S][lines][ldk] + exponents [NP][lines]
-// + the diagonal of the split
+// The shard's slice set, shared by both step directions (equilibrated Ozaki splitting): per real
+// component P, row exponents r[P][i] (row maxima of |H_P|, diagonal excluded) and column
+// exponents c[P][j] (column maxima of |H_P| 2^-r_i) give H_P = D_r Hhat_P D_c with
+// 128 |hhat| < 127.5 in every row and column; Hhat_P is cut into S slices stored [j][i] (i
+// contiguous), which the backward step reads as a K-major operand (A = H^H: row j, k = i) and the
+// forward step as an MN-major one (A = H: m = i, k = j).  21 B per complex element in all (the
+// round-1 design kept one set per direction: 42 B).  The diagonal of the split is kept per
+// direction (forward: H[m][m + off]; backward: conj(H[m - off][m])).
 template <class T>
-static const OzShard& oz_shard(chase_handle* h, int dir, const void* H, int64_t ldh) {
+static const OzShard& oz_shard(chase_handle* h, const void* H, int64_t ldh) {
   constexpr int NP = oz::Comp<T>::NP;
-  OzShard& z = dir == 0 ? h->oz_fwd : h->oz_bwd;
+  OzShard& z = h->oz_fwd;
   const int S = oz_slices_opt(h);
   if (z.src == H && z.ld == ldh && z.S == S && z.slices.p) return z;
   const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
-  const int lines = dir == 0 ? (int)p : (int)q, K = dir == 0 ? (int)q : (int)p;
-  const int64_t ldk = oz::ldk_of(K);
-  z.slices.alloc((size_t)NP * S * lines * ldk);
-  z.exps.alloc(sizeof(int) * NP * (size_t)lines + sizeof(unsigned long long) * NP * (size_t)lines + 16);
-  int* e = z.exps.as<int>();
-  unsigned long long* mx = reinterpret_cast<unsigned long long*>(e + NP * (size_t)lines + (NP * lines & 1));
+  const int64_t ldk = oz::ldk_of(p);
+  z.slices.alloc((size_t)NP * S * q * ldk);
+  // exps: r [NP][p] | c [NP][q] | row maxima (u64) [NP][p]
+  const size_t ri = (size_t)NP * p, ci = (size_t)NP * q;
+  z.exps.alloc(sizeof(int) * (ri + ci) + 16 + sizeof(unsigned long long) * ri);
+  int* r = z.exps.as<int>();
+  int* c = r + ri;
+  unsigned long long* mx = reinterpret_cast<unsigned long long*>(z.exps.as<char>() + ((sizeof(int) * (ri + ci) + 15) & ~size_t(15)));
   const T* Hz = reinterpret_cast<const T*>(H);
-  // diagonal split: global diagonal of H in local coordinates (row i, column i + (r0 - c0))
   const int64_t r0 = h->grid.rows.start, c0 = h->grid.cols.start;
+  // diagonal split: the global diagonal of H sits at local (i, i + (r0 - c0)) = (j + (c0 - r0), j)
+  CHASE_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * ri, h->stream));
+  oz::oz_row_max<T><<<dim3(ceil_div(p, 256), ceil_div(q, 256)), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q,
+                                                                                     (int)(r0 - c0), mx);
+  CHASE_CHECK_LAUNCH();
+  oz::oz_row_exp<T><<<ceil_div(p, 256), 256, 0, h->stream>>>(mx, (int)p, r);
+  CHASE_CHECK_LAUNCH();
   with_S(S, [&](auto Sc) {
-    constexpr int SS = decltype(Sc)::value;
-    if (dir == 0)
-      slice_rows<SS, T>(Hz, ldh, (int)p, (int)q, (int)(r0 - c0), mx, z.slices.as<int8_t>(), ldk, (int64_t)lines * ldk,
-                        e, h->stream);
-    else   // A = H^H: line j = column j of H, conjugated; its diagonal element is row j + (c0 - r0)
-      slice_lines<SS, T>(Hz, ldh, (int)p, (int)q, true, (int)(c0 - r0), z.slices.as<int8_t>(), ldk,
-                         (int64_t)lines * ldk, e, h->stream);
+    slice_lines<decltype(Sc)::value, T>(Hz, ldh, (int)p, (int)q, 1, (int)(c0 - r0), r, (int)p, -1, z.slices.as<int8_t>(),
+                                        ldk, (int64_t)q * ldk, c, h->stream);
   });
-  z.diag.alloc(sizeof(double2) * (size_t)lines);
-  oz::oz_diag<T><<<ceil_div(lines, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, dir, (int)(r0 - c0),
-                                                             z.diag.as<double2>());
+  z.diag.alloc(sizeof(double2) * (size_t)(p + q));
+  oz::oz_diag<T><<<ceil_div(p, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, 0, (int)(r0 - c0),
+                                                          z.diag.as<double2>());
+  CHASE_CHECK_LAUNCH();
+  oz::oz_diag<T><<<ceil_div(q, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, 1, (int)(r0 - c0),
+                                                          z.diag.as<double2>() + p);
   CHASE_CHECK_LAUNCH();
   z.src = H;
   z.ld = ldh;
@@ -675,7 +659,10 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   constexpr int NP = oz::Comp<T>::NP;
   const int S = oz_slices_opt(h);
   const int dir = d.conjA ? 1 : 0;
-  const OzShard& A = oz_shard<T>(h, dir, d.A, d.lda);
+  const OzShard& A = oz_shard<T>(h, d.A, d.lda);
+  const int64_t pp = h->grid.rows.len, qq = h->grid.cols.len;
+  const int* r_exp = A.exps.as<int>();
+  const int* c_exp = r_exp + (size_t)NP * pp;
   const int M = d.M, N = d.N, K = d.K;
   if (M <= 0 || N <= 0) return;
   cudaStream_t st = h->stream;
@@ -684,8 +671,11 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   h->oz_b.alloc((size_t)NP * S * N * ldkb + sizeof(int) * NP * (size_t)N + 64);
   int8_t* bsl = h->oz_b.as<int8_t>();
   int* fB = reinterpret_cast<int*>(bsl + (size_t)NP * S * N * ldkb);
+  // B' = D X: forward scales X's rows (k = j) by 2^c_j, backward W's rows (k = i) by 2^r_i; the
+  // backward's third component is Wr - Wi (see oz_combine)
   with_S(S, [&](auto Sc) {
-    slice_lines<decltype(Sc)::value, T>(reinterpret_cast<const T*>(d.B), d.ldb, K, N, false, INT_MIN, bsl, ldkb,
+    slice_lines<decltype(Sc)::value, T>(reinterpret_cast<const T*>(d.B), d.ldb, K, N, dir == 0 ? 1 : -1, INT_MIN,
+                                        dir == 0 ? c_exp : r_exp, dir == 0 ? (int)qq : (int)pp, 1, bsl, ldkb,
                                         (int64_t)N * ldkb, fB, st);
   });
   // FP64 accumulators of the real products
@@ -694,8 +684,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   static unsigned long long attr = 0;
   if (first_on_device(attr))
     CHASE_CUDA(cudaFuncSetAttribute(oz::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
-  const int lines_a = M;
-  const int64_t ldka = oz::ldk_of(K);
+  const int64_t ldka = oz::ldk_of(pp);           // slices [j][i], row length ldk(p)
   int cap = oz::MAX_PAIRS;                                  // pairs per launch (see the packing below)
   static const int cap_env = [] { const char* e = std::getenv("CHASE_OZ_PAIRS"); return e ? std::atoi(e) : 0; }();
   if (cap_env > 0) cap = std::min(cap, cap_env);          // tuning knob: slice pairs per launch
@@ -713,7 +702,8 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   const int grid = 2 * std::min(ptiles, sms / 2);            // persistent: one CTA pair per 2 SMs
   for (int P = 0; P < NP; ++P) {
     CUtensorMap ta, tb;
-    oz::make_slice_tmap(&ta, A.slices.as<int8_t>() + (size_t)P * S * lines_a * ldka, K, lines_a, ldka, S, oz::BM);
+    // [P][s][j][i]: dims {p (i, inner), q (j), S}; box {128, 128, 1} serves both directions
+    oz::make_slice_tmap(&ta, A.slices.as<int8_t>() + (size_t)P * S * qq * ldka, pp, qq, ldka, S, oz::BM);
     oz::make_slice_tmap(&tb, bsl + (size_t)P * S * N * ldkb, K, N, ldkb, S, oz::BN / 2);
     bool first = true;
     for (int dsum = 2; dsum <= S + 1; ++dsum) {
@@ -744,6 +734,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
         prm.ldo = M;
         prm.accumulate = first ? 0 : 1;
         prm.hint = hint_env;
+        prm.amn = dir == 0 ? 1 : 0;
         prm.sync = nullptr;
         if (sync_env) {
           CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, st));
@@ -755,7 +746,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
       }
     }
   }
-  const int* eA = A.exps.as<int>();
+  const int* eA = dir == 0 ? r_exp : c_exp;        // output row exponents
   // intersection rows of this direction (the diagonal split and the shift live there)
   const Grid& g = h->grid;
   const int64_t r0 = g.rows.start, c0 = g.cols.start, p = g.rows.len, q = g.cols.len;
@@ -768,7 +759,8 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   }
   oz::oz_combine<T><<<148 * 8, 256, 0, st>>>(Tacc, M, (int64_t)M * N, eA, M, fB, N, reinterpret_cast<T*>(d.C), d.ldc,
                                              d.alpha, d.beta, d.beta != 0.0 ? 1 : 0, reinterpret_cast<const T*>(d.B),
-                                             d.ldb, A.diag.as<double2>(), dlo, std::max(dlo, dhi), doff, d.gamma);
+                                             d.ldb, A.diag.as<double2>() + (dir == 0 ? 0 : pp), dlo, std::max(dlo, dhi),
+                                             doff, d.gamma, dir);
   CHASE_CHECK_LAUNCH();
 }
 
@@ -778,7 +770,7 @@ void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
 }
 
 void ozaki_release(chase_handle* h) {
-  for (OzShard* z : {&h->oz_fwd, &h->oz_bwd}) {
+  for (OzShard* z : {&h->oz_fwd}) {
     z->slices.release();
     z->exps.release();
     z->diag.release();
