@@ -21,7 +21,7 @@ from chase_gen.device import DeviceG2  # noqa: E402
 def main():
     N, nev, nex = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
     fam, dtype, tol = sys.argv[4], sys.argv[5], float(sys.argv[6])
-    max_iter = int(sys.argv[7]) if len(sys.argv) > 7 else 100
+    max_iter = int(sys.argv[7]) if len(sys.argv) > 7 else 0          # 0: auto (library default)
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -58,7 +58,10 @@ def main():
                           "filter_tflops_per_gpu": 8.0 * N * N * rep["matvecs"] / world / max(rep["t_filter"], 1e-12) / 1e12,
                           "eig_err_rel_normH": float(np.max(err) / normH),
                           "eig_err_rel_max": float(np.max(err / np.maximum(np.abs(lam[:nev]), 1e-300))),
-                          "mixed_filter": float(os.environ.get("CHASE_MIXED", "0"))}), flush=True)
+                          "mixed_filter": float(os.environ.get("CHASE_MIXED", "0")),
+                          "options": "defaults (fp64_emulation 7 = Ozaki INT8 emulation for complex double, max_iter auto)"
+                                     if max_iter == 0 and not os.environ.get("CHASE_MIXED") else f"max_iter {max_iter}"}),
+              flush=True)
     ch.close()
     dist.barrier()
     dist.destroy_process_group()
