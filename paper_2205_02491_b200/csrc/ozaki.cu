@@ -63,6 +63,8 @@ struct Params {
   int hint;                            // 1: L2 evict_first for A (streamed), evict_last for B (re-read)
   unsigned* sync;                      // round barrier counter (zeroed per launch); null = no barrier
   int amn;                             // 1: A is MN-major (slices [k][m], m contiguous: the forward step)
+  int dbg;                             // experiments only (CHASE_OZ_DBG): 1 = drain without the FP64 RMW,
+                                       // 2 = every k block re-loads k block 0 (no HBM streaming)
 };
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {   // K-major, SWIZZLE_128B, 8-row groups 1 KB apart
@@ -232,13 +234,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const uint32_t fb = mapa0(smem_u32(full + s));
             if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * STAGE_BYTES);
             // A box {128, 128, 1}: K-major coordinates (k, m), MN-major (m, k)
-            const int ac0 = p.amn ? m0 : kt * BK, ac1 = p.amn ? kt * BK : m0;
+            const int kb = (p.dbg & 2) ? 0 : kt * BK;
+            const int ac0 = p.amn ? m0 : kb, ac1 = p.amn ? kb : m0;
             if (p.hint) {
               tma_3d_pair_hint(st, &tA, ac0, ac1, p.sa[q], fb, pol_a);
               tma_3d_pair_hint(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb, pol_b);
             } else {
               tma_3d_pair(st, &tA, ac0, ac1, p.sa[q], fb);
-              tma_3d_pair(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb);
+              tma_3d_pair(st + A_BYTES, &tB, kb, nh, p.tb[q], fb);
             }
           }
         }
@@ -302,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
             : "r"(base + c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (row < p.M) {
+        if (row < p.M && !(p.dbg & 1)) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int n = n0 + c0 + j;
@@ -689,6 +692,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   static const int cap_env = [] { const char* e = std::getenv("CHASE_OZ_PAIRS"); return e ? std::atoi(e) : 0; }();
   if (cap_env > 0) cap = std::min(cap, cap_env);          // tuning knob: slice pairs per launch
   static const int hint_env = [] { const char* e = std::getenv("CHASE_OZ_HINT"); return e ? std::atoi(e) : 0; }();
+  static const int dbg_env = [] { const char* e = std::getenv("CHASE_OZ_DBG"); return e ? std::atoi(e) : 0; }();
   static const int sync_env = [] { const char* e = std::getenv("CHASE_OZ_SYNC"); return e ? std::atoi(e) : 1; }();
   h->oz_sync.alloc(256);
   if (16129LL * K > 2147483647LL) throw UsageError("fp64_emulation: K > 133143 needs K chunking (not built)");
@@ -735,6 +739,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
         prm.accumulate = first ? 0 : 1;
         prm.hint = hint_env;
         prm.amn = dir == 0 ? 1 : 0;
+        prm.dbg = dbg_env;
         prm.sync = nullptr;
         if (sync_env) {
           CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, st));
