@@ -66,7 +66,7 @@ struct DBuf {
 struct Options {
   int deg_max = 36;
   int max_iter = 0;             // 0 = auto: iterate while converging (stall_iter rule), cap kAutoIterCap
-  int stall_iter = 30;          // auto: stop after this many iterations without progress
+  int stall_iter = 100;         // auto: stop after this many iterations without progress
   int lanczos_steps = 25;
   int lanczos_runs = 4;
   uint64_t seed_v = 2;
