@@ -671,7 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
 // a = npair / gw groups of gw, group g walks the m tiles g, g + a, ... of segment 0, then of
 // segment 1, ..., and pair j of the group always takes n tile seg gw + j.  The gw pairs of a group
 // stream one A panel (the big H shard) in lockstep, and a round barrier of the TMA producers
-// (200 us timeout: performance only, never correctness) keeps the groups in step, so the B panels
+// (50 ms timeout: performance only, never correctness) keeps the groups in step, so the B panels
 // of the segment are shared too.  (Panels are K long -- far beyond L2 at large shards -- so a
 // round costs a + gw panel reads: 17 for 8 x 9 vs 34 for 2 x 32 at N = 170000 / 2 x 2.)  The chunk
 // accumulators stay double-buffered across tiles (global chunk counter), so the next tile's first
@@ -752,7 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C64_THREADS, 1)
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sync) : "memory");
             if (v >= target) break;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 200000ull) { sync = nullptr; break; }
+            if (t1 - t0 > 50000000ull) { sync = nullptr; break; }
           }
         }
         int tmi, tni;

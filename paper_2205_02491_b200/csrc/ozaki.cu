@@ -208,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // together, so the pairs stream the A and B k windows in step and share them through L2
           // (B, re-read by every m round, does not fit L2; without the barrier the pairs drift
           // apart over a launch -- measured 35 GB vs 13 GB of DRAM reads per launch).  The
-          // results never depend on it: a CTA that waits longer than 200 us (e.g. not all CTAs
+          // results never depend on it: a CTA that waits longer than 50 ms (e.g. not all CTAs
           // resident because another kernel shares the GPU) stops synchronising and carries on.
           target += 2u * (unsigned)tiles_n * (unsigned)min(ngroups, tiles_m - r * ngroups);
           atomicAdd(p.sync, 1u);
@@ -219,7 +219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync) : "memory");
             if (v >= target) break;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 200000ull) { p.sync = nullptr; break; }
+            if (t1 - t0 > 50000000ull) { p.sync = nullptr; break; }
           }
         }
         int tmi, tni;
