@@ -258,8 +258,10 @@ def projected_oracle_tts(rate_tflops, cases):
 def _recorded_tts():
     """Measured (matvecs, iterations) of the large configs from committed GPU runs (profiles/)."""
     cases = []
-    for f, cfg in (("r01_config4_121_4gpu_tts.json", "config4 1-2-1"),
-                   ("r01_config4_wilkinson_4gpu_tts.json", "config4 Wilkinson")):
+    for f, cfg in (("r02_config4_121_4gpu_tts.json", "config4 1-2-1"),
+                   ("r02_config4_wilkinson_4gpu_tts.json", "config4 Wilkinson")):
+        if not os.path.exists(os.path.join(ROOT, "profiles", f)):
+            f = f.replace("r02_", "r01_")                     # round-1 (DMMA path) record
         try:
             lines = [ln for ln in open(os.path.join(ROOT, "profiles", f)) if ln.startswith("{")]
             d = json.loads(lines[-1])
