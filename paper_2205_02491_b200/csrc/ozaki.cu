@@ -44,13 +44,22 @@
 namespace chase {
 
 namespace oz {
-constexpr int BM = 128, BN = 256, BK = 128;            // per CTA: 128 rows; per pair: 256 x 256; BK int8 (= bytes)
-constexpr uint32_t A_BYTES = BM * BK, B_BYTES = (BN / 2) * BK, STAGE_BYTES = A_BYTES + B_BYTES;   // 16 + 16 KB
-constexpr int STAGES = 6;
-constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+constexpr int BM = 128, BN = 256, BK = 128;            // per CTA: 128 rows; per MMA: 256 x 256; BK int8 (= bytes)
+constexpr uint32_t A_BYTES = BM * BK, B_BYTES = (BN / 2) * BK;   // 16 KB of A rows, 16 KB of B columns per sub-tile
 constexpr int THREADS = 192;
 constexpr int MAX_PAIRS = 8;
-constexpr uint32_t TCOLS = 2 * BN;                      // two 256-column int32 accumulators (double buffer)
+constexpr uint32_t TCOLS = 512;                         // all of TMEM: NS = 1 two 256-col buffers, NS = 2 one 512-col
+// NS = 256-column sub-tiles per pair tile (1: 256 x 256 tiles, double-buffered accumulators --
+// the default; 2: 256 x 512 tiles, one accumulator: each A k block feeds two MMAs, so the TMA
+// writes per MAC drop from 60 to 44 B/clk/SM and a round re-reads half as many B panels, but it
+// measured 15 % slower -- the exposed drain and the 4-stage ring cost more; CHASE_OZ_NS=2)
+template <int NS> struct Shape {
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + NS * B_BYTES;
+  static constexpr int STAGES = NS == 1 ? 6 : 4;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024;
+  static constexpr int BNT = NS * BN;                    // tile width
+  static constexpr int NBUF = 2 / NS;                    // TMEM accumulator buffers
+};
 
 struct Params {
   int M, N, K;
@@ -140,15 +149,18 @@ __device__ __forceinline__ void commit_both(uint64_t* bar) {
 // 256-column TMEM accumulators, so the drain of tile t overlaps the MMAs of tile t + 1.  Drain:
 // 4 warps per CTA (TMEM lane quadrant = warp % 4), 16 columns at a time, 2^-7d x acc added
 // into the FP64 output.
+template <int NS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, Params p) {
+  constexpr uint32_t STAGE_BYTES = Shape<NS>::STAGE_BYTES;
+  constexpr int STAGES = Shape<NS>::STAGES, BNT = Shape<NS>::BNT, NBUF = Shape<NS>::NBUF;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + 2 * BM - 1) / (2 * BM);
+  const int tiles_n = (p.N + BNT - 1) / BNT, tiles_m = (p.M + 2 * BM - 1) / (2 * BM);
   const int pair = blockIdx.x >> 1, npair = gridDim.x >> 1;
   const int KT = (p.K + BK - 1) / BK;
   // Static L2-aware schedule: the pairs form groups of tiles_n; group g walks the m tiles
@@ -225,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         int tmi, tni;
         tile_mn(r, tmi, tni);
         const int m0 = tmi * 2 * BM + (int)rank * BM;
-        const int nh = tni * BN + (int)rank * (BN / 2);
+        const int nh = tni * BNT + (int)rank * (BN / 2);      // this CTA's half of sub-tile 0
         for (int kt = 0; kt < KT; ++kt) {
           for (int q = 0; q < p.npairs; ++q, ++it) {
             const int s = it % STAGES;
@@ -238,10 +250,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const int ac0 = p.amn ? m0 : kb, ac1 = p.amn ? kb : m0;
             if (p.hint) {
               tma_3d_pair_hint(st, &tA, ac0, ac1, p.sa[q], fb, pol_a);
-              tma_3d_pair_hint(st + A_BYTES, &tB, kt * BK, nh, p.tb[q], fb, pol_b);
+#pragma unroll
+              for (int sub = 0; sub < NS; ++sub)
+                tma_3d_pair_hint(st + A_BYTES + sub * B_BYTES, &tB, kb, nh + sub * BN, p.tb[q], fb, pol_b);
             } else {
               tma_3d_pair(st, &tA, ac0, ac1, p.sa[q], fb);
-              tma_3d_pair(st + A_BYTES, &tB, kb, nh, p.tb[q], fb);
+#pragma unroll
+              for (int sub = 0; sub < NS; ++sub)
+                tma_3d_pair(st + A_BYTES + sub * B_BYTES, &tB, kb, nh + sub * BN, p.tb[q], fb);
             }
           }
         }
@@ -256,12 +272,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
       int it = 0, tl = 0;
       for (int r = 0; r < NT; ++r, ++tl) {
-        const int b = tl & 1;
-        if (tl >= 2) {
-          wait_cluster(acc_empty + b, ((tl >> 1) - 1) & 1);
+        const int b = tl % NBUF;
+        if (tl >= NBUF) {
+          wait_cluster(acc_empty + b, ((tl / NBUF) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
         }
-        const uint32_t td = tm + (uint32_t)b * BN;
+        const uint32_t td = tm + (uint32_t)b * BNT;
         for (int j = 0; j < KT * p.npairs; ++j, ++it) {
           const int s = it % STAGES;
           mbar_wait(full + s, (it / STAGES) & 1);
@@ -271,10 +287,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < BK / 32; ++kk) {
               const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
-              asm volatile(
-                  "{ .reg .pred q; setp.ne.b32 q, %4, 0; tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, q; }"
-                  ::"r"(td), "l"(p.amn ? sdesc_mn(sa + kk * 4096) : sdesc(sa + kk * 32)), "l"(sdesc(sb + kk * 32)),
-                    "r"(idesc), "r"(acc));
+              const uint64_t da = p.amn ? sdesc_mn(sa + kk * 4096) : sdesc(sa + kk * 32);
+#pragma unroll
+              for (int sub = 0; sub < NS; ++sub)
+                asm volatile(
+                    "{ .reg .pred q; setp.ne.b32 q, %4, 0; tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, q; }"
+                    ::"r"(td + sub * BN), "l"(da), "l"(sdesc(sb + sub * B_BYTES + kk * 32)), "r"(idesc), "r"(acc));
             }
             commit_both(empty + s);
           }
@@ -289,15 +307,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t lane_off = (uint32_t)(32 * quad) << 16;
     int tl = 0;
     for (int r = 0; r < NT; ++r, ++tl) {
-      const int b = tl & 1;
+      const int b = tl % NBUF;
       int tmi, tni;
       tile_mn(r, tmi, tni);
       const int row = tmi * 2 * BM + (int)rank * BM + 32 * quad + lane;
-      const int n0 = tni * BN;
-      mbar_wait(acc_full + b, (tl >> 1) & 1);
+      const int n0 = tni * BNT;
+      mbar_wait(acc_full + b, (tl / NBUF) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t base = tm + lane_off + (uint32_t)b * BN;
-      for (int c0 = 0; c0 < BN; c0 += 16) {
+      const uint32_t base = tm + lane_off + (uint32_t)b * BNT;
+      for (int c0 = 0; c0 < BNT; c0 += 16) {
         uint32_t r[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -684,9 +702,17 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   // FP64 accumulators of the real products
   h->oz_t.alloc(sizeof(double) * NP * (size_t)M * N);
   double* Tacc = h->oz_t.as<double>();
-  static unsigned long long attr = 0;
-  if (first_on_device(attr))
-    CHASE_CUDA(cudaFuncSetAttribute(oz::oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)oz::SMEM));
+  static unsigned long long attr1 = 0, attr2 = 0;
+  if (first_on_device(attr1))
+    CHASE_CUDA(cudaFuncSetAttribute(oz::oz_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz::Shape<1>::SMEM));
+  if (first_on_device(attr2))
+    CHASE_CUDA(cudaFuncSetAttribute(oz::oz_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)oz::Shape<2>::SMEM));
+  static const int ns_env = [] { const char* e = std::getenv("CHASE_OZ_NS"); return e ? std::atoi(e) : 0; }();
+  // 256 x 512 tiles (NS = 2) measured slower at the bench shape (87-89 vs 104-105 TFLOP/s: one
+  // accumulator leaves the drain exposed and 4 stages hide less latency), so NS = 1 is the default
+  const int ns = ns_env == 2 && N > oz::BN ? 2 : 1;
   const int64_t ldka = oz::ldk_of(pp);           // slices [j][i], row length ldk(p)
   int cap = oz::MAX_PAIRS;                                  // pairs per launch (see the packing below)
   static const int cap_env = [] { const char* e = std::getenv("CHASE_OZ_PAIRS"); return e ? std::atoi(e) : 0; }();
@@ -696,7 +722,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   static const int sync_env = [] { const char* e = std::getenv("CHASE_OZ_SYNC"); return e ? std::atoi(e) : 1; }();
   h->oz_sync.alloc(256);
   if (16129LL * K > 2147483647LL) throw UsageError("fp64_emulation: K > 133143 needs K chunking (not built)");
-  const int ptiles = ceil_div(M, 2 * oz::BM) * ceil_div(N, oz::BN);
+  const int ptiles = ceil_div(M, 2 * oz::BM) * ceil_div(N, ns * oz::BN);
   int sms = 148;
   {
     int dev = 0;
@@ -746,7 +772,8 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
           prm.sync = h->oz_sync.as<unsigned>();
         }
         first = false;
-        oz::oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(ta, tb, prm);
+        if (ns == 2) oz::oz_gemm_kernel<2><<<grid, oz::THREADS, oz::Shape<2>::SMEM, st>>>(ta, tb, prm);
+        else oz::oz_gemm_kernel<1><<<grid, oz::THREADS, oz::Shape<1>::SMEM, st>>>(ta, tb, prm);
         CHASE_CHECK_LAUNCH();
       }
     }
