@@ -203,7 +203,7 @@ void c64_step_bn(chase_handle* h, int dir, const void* H, int64_t ldh, const voi
       if (gw_env > 0 && tiles_n % gw_env == 0 && gw_env <= gridp / 2) gw = gw_env;   // tuning knob
       h->oz_sync.alloc(256);
       CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, h->stream));
-      unsigned* sy = h->oz_sync.as<unsigned>();
+      unsigned* sy = h->colocated ? nullptr : h->oz_sync.as<unsigned>();   // co-located ranks share the SMs
       auto gp = [&](auto kern, int slot) {
         if (first_on_device(attrp[slot]))
           CHASE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));

@@ -767,7 +767,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
         prm.amn = dir == 0 ? 1 : 0;
         prm.dbg = dbg_env;
         prm.sync = nullptr;
-        if (sync_env) {
+        if (sync_env && !h->colocated) {     // co-located ranks share the SMs: no round barrier
           CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, st));
           prm.sync = h->oz_sync.as<unsigned>();
         }
