@@ -155,3 +155,24 @@ def test_real_emulated_solve():
     assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
     V = vecs.cpu().numpy()[:, :nev]
     assert np.max(np.linalg.norm(H @ V - V * vals[None, :], axis=0)) <= 1e-10 * normH
+
+
+@pytest.mark.parametrize("direction", [0, 1])
+def test_emulated_step_graded_matrix(direction):
+    """A graded Hermitian H = D A D (D spanning 1e-6 .. 1) and a graded block X: the row / column
+    power-of-two equilibration of the splitting keeps the step at the complex-double bar."""
+    import paper_2205_02491_b200 as pkg
+    N, n = 640, 48
+    rng = np.random.default_rng(11)
+    A = make_matrix("uniform", N, "g2", seed=3).dense()
+    d = np.logspace(-6, 0, N)
+    H = (d[:, None] * A) * d[None, :]
+    X = (rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))) * np.logspace(0, -4, n)[None, :]
+    Y0 = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
+    ref = oracle.hemm_step(H, X, Y0 * 1e-6, 0.9, 0.5, 1e-3)
+    ch = pkg.Chase(N, n, 1)
+    dY = _dev(Y0 * 1e-6)
+    ch.hemm_step(direction, _dev(H), _dev(X), dY, n, 0.9, 0.5, 1e-3)
+    out = dY.cpu().numpy()
+    colerr = np.linalg.norm(out - ref, axis=0) / np.linalg.norm(ref, axis=0)
+    assert np.max(colerr) <= 1e-13, float(np.max(colerr))
