@@ -105,7 +105,9 @@ chase_status chase_init(chase_handle** out, const chase_init_args* args);
 /* Options (defaults): deg_max=36, max_iter=0 (auto: iterate while the solve progresses -- a new
  * locked pair or the smallest active residual below 0.99 x its best so far -- and return
  * CHASE_E_MAXITER after stall_iter=100 iterations without progress, or 5000 in all; a value > 0
- * is a hard cap), lanczos_steps=25, lanczos_runs=4, seed_v=2,
+ * is a hard cap), deg_extra=2 (degrees added to the optimal-degree estimate before the cap --
+ * the estimate aims exactly at tol and otherwise lets columns just above tol creep),
+ * lanczos_steps=25, lanczos_runs=4, seed_v=2,
  * seed_lanczos=3, largest=0, approx=0 (1: ritz_vectors holds an initial V-hat on entry),
  * gemm3m=1 (filter and H*Q products use the 3M complex product -- 3 real DMMAs per complex
  * multiply-add instead of 4; normwise-stable; 0 selects the 4M kernel),

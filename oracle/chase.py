@@ -216,10 +216,13 @@ def residual_norms(HV, V, theta):
 # ----------------------------------------------------------------------------------------------
 # Degrees (Alg. 1 line 12), locking (line 8), bounds (line 9), sort (line 14)
 # ----------------------------------------------------------------------------------------------
-def optimal_degrees(tol, res, theta, c, e, deg_max=36):
+def optimal_degrees(tol, res, theta, c, e, deg_max=36, extra=0):
     """m_a <- Degrees(tol, Res_a, lambda_a, c, e)  (Alg. 1 line 12).  Ledger #4:
     t_a = (c - theta_a)/e; rho_a = max |t_a +- sqrt(t_a^2 - 1)|; m_a = cap if |t_a| <= 1, else
-    clamp(ceil(ln(res_a/tol)/ln rho_a), 1, cap); then rounded up to even."""
+    clamp(ceil(ln(res_a/tol)/ln rho_a), 1, cap); then rounded up to even.
+    `extra` (reading 4b; "may differ in constants"): degrees added to the estimate
+    before the cap -- the estimate aims exactly at tol, so a column just above tol gets m -> 1 and
+    creeps (measured: 100+ iterations at res = 1.01 tol); chase_solve uses extra = 2."""
     res = np.atleast_1d(np.asarray(res, dtype=np.float64))
     theta = np.atleast_1d(np.asarray(theta, dtype=np.float64))
     cap_even = deg_max - (deg_max % 2)
@@ -233,7 +236,7 @@ def optimal_degrees(tol, res, theta, c, e, deg_max=36):
             rho = max(abs(t + s), abs(t - s))
             ratio = res[a] / tol
             m = math.ceil(math.log(ratio) / math.log(rho)) if ratio > 0 else 1
-            m = min(max(m, 1), deg_max)
+            m = min(max(m, 1) + extra, deg_max)
         m = m + (m % 2)
         out[a] = min(m, cap_even) if deg_max >= 2 else m
     return out
@@ -265,7 +268,7 @@ class Report:
 
 
 def chase_solve(H, nev: int, nex: int, deg: int = 20, tol: float = 1e-10, deg_max: int = 36,
-                max_iter: int = 100, lanczos_steps: int = 25, lanczos_runs: int = 4,
+                max_iter: int = 100, lanczos_steps: int = 25, lanczos_runs: int = 4, deg_extra: int = 2,
                 seed_v: int = 2, seed_lanczos: int = 3, largest: bool = False, V0=None,
                 lanczos_res: LanczosResult | None = None):
     """Alg. 1, serial semantics.  Returns (eigenvalues[nev] ascending,
@@ -314,7 +317,7 @@ def chase_solve(H, nev: int, nex: int, deg: int = 20, tol: float = 1e-10, deg_ma
         if locked >= nev:
             break
         act = slice(locked, n_e)
-        m = optimal_degrees(tol, res[act], ritz[act], c, e, deg_max)   # lines 11-13
+        m = optimal_degrees(tol, res[act], ritz[act], c, e, deg_max, deg_extra)   # lines 11-13
         order = np.argsort(m, kind="stable")                            # line 14
         V[:, act] = V[:, act][:, order]
         ritz[act] = ritz[act][order]

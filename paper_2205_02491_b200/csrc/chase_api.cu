@@ -554,6 +554,7 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     if (!key) throw UsageError("null option key");
     std::string k(key);
     if (k == "deg_max") { if (v < 2) throw UsageError("deg_max >= 2"); h->opt.deg_max = (int)v; }
+    else if (k == "deg_extra") { if (v < 0) throw UsageError("deg_extra >= 0"); h->opt.deg_extra = (int)v; }
     else if (k == "max_iter") { if (v < 0) throw UsageError("max_iter >= 0 (0 = auto)"); h->opt.max_iter = (int)v; }
     else if (k == "stall_iter") { if (v < 1) throw UsageError("stall_iter >= 1"); h->opt.stall_iter = (int)v; }
     else if (k == "lanczos_steps") { if (v < 2) throw UsageError("lanczos_steps >= 2"); h->opt.lanczos_steps = (int)v; }

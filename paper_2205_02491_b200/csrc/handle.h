@@ -65,6 +65,7 @@ struct DBuf {
 
 struct Options {
   int deg_max = 36;
+  int deg_extra = 2;            // degrees added to the optimal-degree estimate (reading 4b)
   int max_iter = 0;             // 0 = auto: iterate while converging (stall_iter rule), cap kAutoIterCap
   int stall_iter = 100;         // auto: stop after this many iterations without progress
   int lanczos_steps = 25;

@@ -32,7 +32,10 @@ namespace chase {
 namespace {
 
 // m_a <- Degrees(tol, Res_a, lambda_a, c, e)  (Alg. 1 line 12; ledger #4 / S:366)
-int optimal_degree(double tol, double res, double theta, double c, double e, int deg_max) {
+// deg_extra (reading 4b): degrees added to the estimate before the cap -- it aims at
+// exactly tol, so a column just above tol would get m -> 1 and creep (measured on config 3:
+// 100+ iterations at res = 1.01 tol).
+int optimal_degree(double tol, double res, double theta, double c, double e, int deg_max, int deg_extra) {
   const double t = (c - theta) / e;
   int m;
   if (std::fabs(t) <= 1.0) {
@@ -42,7 +45,7 @@ int optimal_degree(double tol, double res, double theta, double c, double e, int
     const double rho = std::max(std::fabs(t + s), std::fabs(t - s));
     const double ratio = res / tol;
     m = ratio > 0.0 ? (int)std::ceil(std::log(ratio) / std::log(rho)) : 1;
-    m = std::min(std::max(m, 1), deg_max);
+    m = std::min(std::max(m, 1) + deg_extra, deg_max);
   }
   m += (m & 1);
   const int cap_even = deg_max - (deg_max & 1);
@@ -369,7 +372,7 @@ static chase_status solve_t(chase_handle* h, const void* Hv, int64_t ldh, int ne
     // ---- lines 11-14: degrees, stable sort by degree
     const int na = n_e - locked;
     std::vector<int> mm(na), perm(na);
-    for (int a = 0; a < na; ++a) mm[a] = optimal_degree(tol_deg, res[locked + a], ritz[locked + a], c, e, deg_max);
+    for (int a = 0; a < na; ++a) mm[a] = optimal_degree(tol_deg, res[locked + a], ritz[locked + a], c, e, deg_max, h->opt.deg_extra);
     std::iota(perm.begin(), perm.end(), 0);
     std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return mm[x] < mm[y]; });
     std::vector<double> rz(na), rs(na);

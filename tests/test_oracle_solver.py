@@ -225,3 +225,15 @@ def test_solve_real_symmetric(fam, kind):
     vals, vecs, rep = oracle.chase_solve(H, 30, 10, tol=1e-10)
     assert vecs.dtype == np.float64
     _check_solution(M, vals, vecs, rep, 30, 1e-10, H)
+
+
+def test_degrees_extra_margin_hand_values():
+    """Reading 4b: `extra` degrees are added to the estimate before the cap and the
+    even rounding.  t = 1.5: rho = 1.5 + sqrt(1.25) = 2.618...; res/tol = 1e3 -> ln 1e3 / ln rho =
+    7.18 -> 8 (+2 -> 10); res/tol = 1.01 -> 0.0103 -> 1 -> even 2 (+2 -> 3 -> even 4); the cap
+    still binds (res/tol = 1e30 -> 72 -> cap 36)."""
+    tol, e = 1e-10, 1.0
+    c = 1.5                      # theta = 0 -> t = 1.5
+    for ratio, base, plus2 in ((1e3, 8, 10), (1.01, 2, 4), (1e30, 36, 36)):
+        assert int(oracle.optimal_degrees(tol, [ratio * tol], [0.0], c, e, 36)[0]) == base
+        assert int(oracle.optimal_degrees(tol, [ratio * tol], [0.0], c, e, 36, extra=2)[0]) == plus2
