@@ -80,6 +80,7 @@ struct Options {
   bool fused_reduce_c64 = false;  // f1 for the complex-single filter (measured slower than NCCL + rebuild)
   double peer_timeout = 120.0;    // f1: seconds a rank waits for its peers' tiles before failing
   double comm_timeout = 0.0;      // host waits poll ncclCommGetAsyncError; > 0: also fail after this many s
+  double oz_gemm_min = 4e9;       // plain iteration GEMMs with M N K >= this also run on the emulation
   int fp64_emulation = 7;         // f4: > 0 = complex-double filter products on INT8 tensor cores (Ozaki, S slices)
 };
 
@@ -111,7 +112,7 @@ struct chase_handle {
     int64_t ld = 0;
     int S = 0;
     chase::DBuf slices, exps, diag;
-  } oz_fwd;
+  } oz_fwd, oz_g;                     // the shard's set; the A operand of a general emulated GEMM
   bool oz_off = false;                 // fp64_emulation fell back to DMMA (slices did not fit)
   chase::DBuf oz_b, oz_t, oz_sync;     // fp64_emulation: slices of the block X, FP64 product accumulators
   const void* h32_src = nullptr;
@@ -194,6 +195,8 @@ void peer_check(chase_handle* h);
 void peer_release(chase_handle* h);
 // f4 (ozaki.cu): one local fused step with the complex products emulated on INT8 tensor cores
 void ozaki_step(chase_handle* h, const ZgemmDesc& d);
+// a general C = alpha op(A) B + beta C on the emulation (no shift, no triangular B, no fused reduce)
+void ozaki_gemm(chase_handle* h, const ZgemmDesc& d);
 void ozaki_release(chase_handle* h);
 // tile count of one fused step fits the arrival counters (else the step all-reduces with NCCL)
 bool peer_tiles_fit(int tiles);

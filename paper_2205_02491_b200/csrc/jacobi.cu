@@ -53,14 +53,54 @@ __global__ void k_pad_init(const double2* G, int64_t ldg, int n, double2* A, dou
   }
 }
 
+// pair i of parallel step r of the circle method over S players (player S-1 fixed), p < q
+__device__ __forceinline__ void pair_of(int r, int i, int& p, int& q) {
+  if (i == 0) { p = r; q = S - 1; }
+  else { p = (r + i) % (S - 1); q = (r - i + (S - 1)) % (S - 1); }
+  if (p > q) { const int tmp = p; p = q; q = tmp; }
+}
+
+// U <- U J for one parallel step: items (row i, pair cb), 64 x 32 of them, item0, item0 + stride,
+// ... (at most 3 per thread: all loads first, so the items' latencies overlap)
+__device__ __forceinline__ void jacobi_u_update(double2* Um, const double* rc, const double* rs, const double2* rph,
+                                                const int* rp, const int* rq, int item0, int stride) {
+  constexpr int LD_ = 2 * 32 + 1;
+  double2 xp[3], xq[3];
+  int at[3][2];
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int idx = item0 + u * stride;
+    if (idx < 64 * 32) {
+      const int i = idx >> 5, cb = idx & 31;
+      at[u][0] = i * LD_ + rp[cb];
+      at[u][1] = i * LD_ + rq[cb];
+      xp[u] = Um[at[u][0]];
+      xq[u] = Um[at[u][1]];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int idx = item0 + u * stride;
+    if (idx < 64 * 32) {
+      const int cb = idx & 31;
+      const double cc = rc[cb], sc = rs[cb];
+      const double2 q = cmul(rph[cb], xq[u]);
+      Um[at[u][0]] = make_double2(cc * xp[u].x - sc * q.x, cc * xp[u].y - sc * q.y);
+      Um[at[u][1]] = make_double2(sc * xp[u].x + cc * q.x, sc * xp[u].y + cc * q.y);
+    }
+  }
+}
+
 // One CTA per pair: diagonalise the 64 x 64 Hermitian subproblem by cyclic Jacobi; write U_k.
-constexpr int SUB_T = 1024;   // 32 rotation pairs x 32 threads
+constexpr int SUB_T = 1024;
+constexpr int NTRI = W * (W + 1) / 2;   // pair blocks (ra <= cb) of one parallel step
 __global__ void __launch_bounds__(SUB_T) k_sub_eig(const double2* A, int np, const int* pairs, double2* U, int max_inner) {
   extern __shared__ double2 sm[];
   double2* Sm = sm;              // S x LD
   double2* Um = sm + S * LD;     // S x LD
-  __shared__ double rc[W], rs[W];
-  __shared__ double2 rph[W];
+  __shared__ double rcb[2][W], rsb[2][W];     // rotations of steps r (buffer r & 1) and r - 1
+  __shared__ double2 rphb[2][W];
+  __shared__ int rpb[2][W], rqb[2][W];
   __shared__ double red[SUB_T];
   const int k = blockIdx.x, t = threadIdx.x;
   for (int idx = t; idx < S * S; idx += SUB_T) {
@@ -69,7 +109,14 @@ __global__ void __launch_bounds__(SUB_T) k_sub_eig(const double2* A, int np, con
     Um[i * LD + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
-  const int pr = t >> 5, sub = t & 31;    // 32 pairs x 32 threads
+  const int pr = t >> 5, sub = t & 31;    // warp, lane
+  // thread t < NTRI owns the pair block (tri_r, tri_c), tri_r <= tri_c (row-major upper triangle)
+  int tri_r = 0, tri_c = 0;
+  if (t < NTRI) {
+    int rem = t;
+    while (rem >= W - tri_r) { rem -= W - tri_r; ++tri_r; }
+    tri_c = tri_r + rem;
+  }
   __shared__ int nrot;
   if (t == 0) nrot = 0;
   __syncthreads();
@@ -109,55 +156,82 @@ __global__ void __launch_bounds__(SUB_T) k_sub_eig(const double2* A, int np, con
     __syncthreads();
     if (t == 0) nrot = 0;
     __syncthreads();
+    // Per parallel step r: (A) warp 0 computes the 32 rotations of step r from S while warps
+    // 1..31 apply the rotations of step r - 1 to U (U's update only feeds the output, so it runs
+    // one step behind, under the rotation math); (B) S <- J_r^H S J_r.
     for (int r = 0; r < S - 1; ++r) {
-      // circle method: player S-1 fixed; pair 0 = (r, S-1); pair i = ((r+i) % 63, (r-i+63) % 63)
-      int p, q;
-      if (pr == 0) { p = r; q = S - 1; }
-      else { p = (r + pr) % (S - 1); q = (r - pr + (S - 1)) % (S - 1); }
-      if (p > q) { const int tmp = p; p = q; q = tmp; }
-      if (sub == 0) {
+      if (pr == 0) {
+        // circle method: player S-1 fixed; pair 0 = (r, S-1); pair i = ((r+i) % 63, (r-i+63) % 63);
+        // lane i: pair i
+        int p, q;
+        pair_of(r, sub, p, q);
         const double a = Sm[p * LD + p].x, d = Sm[q * LD + q].x;
         const double2 b = Sm[p * LD + q];
-        const double ab = hypot(b.x, b.y);
+        const double ab2 = b.x * b.x + b.y * b.y;          // |a_pq|^2 <= ||G||_F^2: no overflow
         double c = 1.0, s = 0.0;
-        double2 ph = make_double2(1.0, 0.0);     // e^{-i phi}
-        // rotate only if |a_pq| is significant relative to the diagonal (Demmel-Veselic)
-        if (ab > 1e-300 && ab > 2e-16 * sqrt(fabs(a) * fabs(d))) {
-          atomicAdd(&nrot, 1);
-          const double tau = (d - a) / (2.0 * ab);
-          const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));
-          c = 1.0 / hypot(1.0, tt);
+        double2 ph = make_double2(1.0, 0.0);               // e^{-i phi}
+        // rotate only if |a_pq| is significant relative to the diagonal (Demmel-Veselic):
+        // |a_pq| > 2e-16 sqrt(|a_pp a_qq|)
+        const bool rot = ab2 >= 2.2250738585072014e-308 && ab2 > 4e-32 * fabs(a) * fabs(d);   // ab2 normal
+        if (rot) {
+          const double inv = rsqrt(ab2);                   // 1 / |a_pq|
+          const double tau = 0.5 * (d - a) * inv;
+          const double at = fabs(tau);
+          // t = sign(tau) / (|tau| + sqrt(1 + tau^2)) (the smaller root; 1 / (2 tau) once tau^2 overflows)
+          const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (at > 1e150 ? 2.0 * at : at + sqrt(1.0 + tau * tau));
+          c = rsqrt(1.0 + tt * tt);
           s = tt * c;
-          ph = make_double2(b.x / ab, -b.y / ab);
+          ph = make_double2(b.x * inv, -b.y * inv);
         }
-        rc[pr] = c; rs[pr] = s; rph[pr] = ph;
+        const unsigned nr = __popc(__ballot_sync(0xffffffffu, rot));
+        if (sub == 0) nrot += (int)nr;
+        const int o = r & 1;
+        rcb[o][sub] = c; rsb[o][sub] = s; rphb[o][sub] = ph; rpb[o][sub] = p; rqb[o][sub] = q;
+      } else if (r > 0) {
+        jacobi_u_update(Um, rcb[(r - 1) & 1], rsb[(r - 1) & 1], rphb[(r - 1) & 1], rpb[(r - 1) & 1],
+                        rqb[(r - 1) & 1], t - 32, SUB_T - 32);
       }
       __syncthreads();
-      const double c = rc[pr], s = rs[pr];
-      const double2 ph = rph[pr];
-      // columns:  x_p' = c x_p - s e^{-i phi} x_q ;  x_q' = s x_p + c e^{-i phi} x_q   (S and U)
-      for (int i = sub; i < S; i += 32) {
-        {
-          const double2 xp = Sm[i * LD + p], xq = cmul(ph, Sm[i * LD + q]);
-          Sm[i * LD + p] = make_double2(c * xp.x - s * xq.x, c * xp.y - s * xq.y);
-          Sm[i * LD + q] = make_double2(s * xp.x + c * xq.x, s * xp.y + c * xq.y);
+      // The 32 rotations are disjoint, so S' = J^H S J splits into 2 x 2 blocks (rows of pair ra,
+      // columns of pair cb; J = [[c, s], [-s e^{-i phi}, c e^{-i phi}]] on (p, q)).  S stays
+      // Hermitian: threads 0..527 take the blocks ra <= cb (columns first, then rows -- the order of
+      // the two-pass form) and store the mirror block as its conjugate transpose.
+      if (t < NTRI) {
+        const int o = r & 1;
+        const int ra = tri_r, cb = tri_c;
+        const int pa = rpb[o][ra], qa = rqb[o][ra], pb = rpb[o][cb], qb = rqb[o][cb];
+        const double ca = rcb[o][ra], sa = rsb[o][ra], cc = rcb[o][cb], sc = rsb[o][cb];
+        const double2 pha = make_double2(rphb[o][ra].x, -rphb[o][ra].y), phb = rphb[o][cb];
+        double2 e[2][2] = {{Sm[pa * LD + pb], Sm[pa * LD + qb]}, {Sm[qa * LD + pb], Sm[qa * LD + qb]}};
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {          // columns:  x_p' = c x_p - s e^{-i phi} x_q ; x_q' = s x_p + c e^{-i phi} x_q
+          const double2 xp = e[x][0], xq = cmul(phb, e[x][1]);
+          e[x][0] = make_double2(cc * xp.x - sc * xq.x, cc * xp.y - sc * xq.y);
+          e[x][1] = make_double2(sc * xp.x + cc * xq.x, sc * xp.y + cc * xq.y);
         }
-        {
-          const double2 xp = Um[i * LD + p], xq = cmul(ph, Um[i * LD + q]);
-          Um[i * LD + p] = make_double2(c * xp.x - s * xq.x, c * xp.y - s * xq.y);
-          Um[i * LD + q] = make_double2(s * xp.x + c * xq.x, s * xp.y + c * xq.y);
+#pragma unroll
+        for (int y = 0; y < 2; ++y) {          // rows:  y_p' = c y_p - s e^{+i phi} y_q ; y_q' = s y_p + c e^{+i phi} y_q
+          const double2 yp = e[0][y], yq = cmul(pha, e[1][y]);
+          e[0][y] = make_double2(ca * yp.x - sa * yq.x, ca * yp.y - sa * yq.y);
+          e[1][y] = make_double2(sa * yp.x + ca * yq.x, sa * yp.y + ca * yq.y);
         }
-      }
-      __syncthreads();
-      // rows:  y_p' = c y_p - s e^{+i phi} y_q ;  y_q' = s y_p + c e^{+i phi} y_q
-      const double2 phc = make_double2(ph.x, -ph.y);
-      for (int j = sub; j < S; j += 32) {
-        const double2 yp = Sm[p * LD + j], yq = cmul(phc, Sm[q * LD + j]);
-        Sm[p * LD + j] = make_double2(c * yp.x - s * yq.x, c * yp.y - s * yq.y);
-        Sm[q * LD + j] = make_double2(s * yp.x + c * yq.x, s * yp.y + c * yq.y);
+        if (ra == cb) {                         // diagonal block: Hermitian by construction
+          e[1][0] = make_double2(e[0][1].x, -e[0][1].y);
+        } else {
+          Sm[pb * LD + pa] = make_double2(e[0][0].x, -e[0][0].y);
+          Sm[qb * LD + pa] = make_double2(e[0][1].x, -e[0][1].y);
+          Sm[pb * LD + qa] = make_double2(e[1][0].x, -e[1][0].y);
+          Sm[qb * LD + qa] = make_double2(e[1][1].x, -e[1][1].y);
+        }
+        Sm[pa * LD + pb] = e[0][0]; Sm[pa * LD + qb] = e[0][1];
+        Sm[qa * LD + pb] = e[1][0]; Sm[qa * LD + qb] = e[1][1];
       }
       __syncthreads();
     }
+    // the last step's rotations on U
+    jacobi_u_update(Um, rcb[(S - 2) & 1], rsb[(S - 2) & 1], rphb[(S - 2) & 1], rpb[(S - 2) & 1], rqb[(S - 2) & 1],
+                    t, SUB_T);
+    __syncthreads();
   }
   double2* Uk = U + (int64_t)k * S * S;
   for (int idx = t; idx < S * S; idx += SUB_T) {

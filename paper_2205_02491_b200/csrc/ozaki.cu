@@ -632,13 +632,13 @@ static void with_S(int S, F&& f) {
 // forward step as an MN-major one (A = H: m = i, k = j).  21 B per complex element in all (the
 // round-1 design kept one set per direction: 42 B).  The diagonal of the split is kept per
 // direction (forward: H[m][m + off]; backward: conj(H[m - off][m])).
+// Slices of a stored p x q matrix (column-major, ld) into z; split = true takes the global
+// diagonal out (local (i, i + off), off = r0 - c0) and records it for the combine.
 template <class T>
-static const OzShard& oz_shard(chase_handle* h, const void* H, int64_t ldh) {
+static void oz_slice_matrix(chase_handle* h, OzShard& z, const void* H, int64_t ldh, int64_t p, int64_t q, bool split,
+                            int64_t off) {
   constexpr int NP = oz::Comp<T>::NP;
-  OzShard& z = h->oz_fwd;
   const int S = oz_slices_opt(h);
-  if (z.src == H && z.ld == ldh && z.S == S && z.slices.p) return z;
-  const int64_t p = h->grid.rows.len, q = h->grid.cols.len;
   const int64_t ldk = oz::ldk_of(p);
   z.slices.alloc((size_t)NP * S * q * ldk);
   // exps: r [NP][p] | c [NP][q] | row maxima (u64) [NP][p]
@@ -648,40 +648,55 @@ static const OzShard& oz_shard(chase_handle* h, const void* H, int64_t ldh) {
   int* c = r + ri;
   unsigned long long* mx = reinterpret_cast<unsigned long long*>(z.exps.as<char>() + ((sizeof(int) * (ri + ci) + 15) & ~size_t(15)));
   const T* Hz = reinterpret_cast<const T*>(H);
-  const int64_t r0 = h->grid.rows.start, c0 = h->grid.cols.start;
-  // diagonal split: the global diagonal of H sits at local (i, i + (r0 - c0)) = (j + (c0 - r0), j)
+  // diagonal split: the global diagonal of H sits at local (i, i + off) = (j - off, j)
+  const int row_diag = split ? (int)off : (1 << 30), col_diag = split ? (int)-off : INT_MIN;
   CHASE_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * ri, h->stream));
   oz::oz_row_max<T><<<dim3(ceil_div(p, 256), ceil_div(q, 256)), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q,
-                                                                                     (int)(r0 - c0), mx);
+                                                                                     row_diag, mx);
   CHASE_CHECK_LAUNCH();
   oz::oz_row_exp<T><<<ceil_div(p, 256), 256, 0, h->stream>>>(mx, (int)p, r);
   CHASE_CHECK_LAUNCH();
   with_S(S, [&](auto Sc) {
-    slice_lines<decltype(Sc)::value, T>(Hz, ldh, (int)p, (int)q, 1, (int)(c0 - r0), r, (int)p, -1, z.slices.as<int8_t>(),
+    slice_lines<decltype(Sc)::value, T>(Hz, ldh, (int)p, (int)q, 1, col_diag, r, (int)p, -1, z.slices.as<int8_t>(),
                                         ldk, (int64_t)q * ldk, c, h->stream);
   });
-  z.diag.alloc(sizeof(double2) * (size_t)(p + q));
-  oz::oz_diag<T><<<ceil_div(p, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, 0, (int)(r0 - c0),
-                                                          z.diag.as<double2>());
-  CHASE_CHECK_LAUNCH();
-  oz::oz_diag<T><<<ceil_div(q, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, 1, (int)(r0 - c0),
-                                                          z.diag.as<double2>() + p);
-  CHASE_CHECK_LAUNCH();
+  if (split) {
+    z.diag.alloc(sizeof(double2) * (size_t)(p + q));
+    oz::oz_diag<T><<<ceil_div(p, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, 0, (int)off, z.diag.as<double2>());
+    CHASE_CHECK_LAUNCH();
+    oz::oz_diag<T><<<ceil_div(q, 256), 256, 0, h->stream>>>(Hz, ldh, (int)p, (int)q, 1, (int)off,
+                                                            z.diag.as<double2>() + p);
+    CHASE_CHECK_LAUNCH();
+  }
+  z.S = S;
+}
+
+// the shard's slice set (cached within one API call, see invalidate_shard_caches)
+template <class T>
+static const OzShard& oz_shard(chase_handle* h, const void* H, int64_t ldh) {
+  OzShard& z = h->oz_fwd;
+  const int S = oz_slices_opt(h);
+  if (z.src == H && z.ld == ldh && z.S == S && z.slices.p) return z;
+  oz_slice_matrix<T>(h, z, H, ldh, h->grid.rows.len, h->grid.cols.len, true, h->grid.rows.start - h->grid.cols.start);
   z.src = H;
   z.ld = ldh;
-  z.S = S;
   return z;
 }
 
 // Y = alpha (op(H) X - gamma E X) + beta Y  (one rank's local part of a fused step; T = double2
 // complex Hermitian, T = double real symmetric)
+// shard = true: A is the handle's H shard (cached slices, diagonal split, shift); false: a general
+// GEMM C = alpha op(A) B + beta C (A sliced for this call, no split, no shift)
 template <class T>
-static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
+static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d, bool shard) {
   constexpr int NP = oz::Comp<T>::NP;
   const int S = oz_slices_opt(h);
   const int dir = d.conjA ? 1 : 0;
-  const OzShard& A = oz_shard<T>(h, d.A, d.lda);
-  const int64_t pp = h->grid.rows.len, qq = h->grid.cols.len;
+  // stored A: shard p x q, or op(A)^{(H)} dims: conjA stores K x M, plain stores M x K
+  const int64_t pp = shard ? h->grid.rows.len : (d.conjA ? d.K : d.M);
+  const int64_t qq = shard ? h->grid.cols.len : (d.conjA ? d.M : d.K);
+  if (!shard) oz_slice_matrix<T>(h, h->oz_g, d.A, d.lda, pp, qq, false, 0);
+  const OzShard& A = shard ? oz_shard<T>(h, d.A, d.lda) : h->oz_g;
   const int* r_exp = A.exps.as<int>();
   const int* c_exp = r_exp + (size_t)NP * pp;
   const int M = d.M, N = d.N, K = d.K;
@@ -789,20 +804,27 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d) {
   } else {
     dlo = (int)std::max<int64_t>(0, r0 - c0); dhi = (int)std::min<int64_t>(q, r0 + p - c0); doff = c0 - r0;
   }
+  if (!shard) dlo = dhi = 0;                            // no split, no shift
   oz::oz_combine<T><<<148 * 8, 256, 0, st>>>(Tacc, M, (int64_t)M * N, eA, M, fB, N, reinterpret_cast<T*>(d.C), d.ldc,
                                              d.alpha, d.beta, d.beta != 0.0 ? 1 : 0, reinterpret_cast<const T*>(d.B),
-                                             d.ldb, A.diag.as<double2>() + (dir == 0 ? 0 : pp), dlo, std::max(dlo, dhi),
-                                             doff, d.gamma, dir);
+                                             d.ldb, shard ? A.diag.as<double2>() + (dir == 0 ? 0 : pp) : nullptr, dlo,
+                                             std::max(dlo, dhi), doff, d.gamma, dir);
   CHASE_CHECK_LAUNCH();
 }
 
 void ozaki_step(chase_handle* h, const ZgemmDesc& d) {
-  if (h->real()) ozaki_step_t<double>(h, d);
-  else ozaki_step_t<double2>(h, d);
+  if (h->real()) ozaki_step_t<double>(h, d, true);
+  else ozaki_step_t<double2>(h, d, true);
+}
+
+void ozaki_gemm(chase_handle* h, const ZgemmDesc& d) {
+  if (d.S || d.red || d.b_upper) throw std::logic_error("ozaki_gemm: plain products only");
+  if (h->real()) ozaki_step_t<double>(h, d, false);
+  else ozaki_step_t<double2>(h, d, false);
 }
 
 void ozaki_release(chase_handle* h) {
-  for (OzShard* z : {&h->oz_fwd}) {
+  for (OzShard* z : {&h->oz_fwd, &h->oz_g}) {
     z->slices.release();
     z->exps.release();
     z->diag.release();

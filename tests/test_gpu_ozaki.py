@@ -176,3 +176,26 @@ def test_emulated_step_graded_matrix(direction):
     out = dY.cpu().numpy()
     colerr = np.linalg.norm(out - ref, axis=0) / np.linalg.norm(ref, axis=0)
     assert np.max(colerr) <= 1e-13, float(np.max(colerr))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "r64"])
+def test_iteration_gemms_on_the_emulation(dtype):
+    """oz_gemm_min = 0 routes every plain GEMM of the iteration (CGS, Gram, RR's Q^H (HQ), Q Z,
+    (HQ) Z) through the INT8 emulation too (only V R^-1 stays on DMMA): the solve keeps the
+    complex-double bars against the exact spectrum and the oracle."""
+    import paper_2205_02491_b200 as pkg
+    real = dtype == "r64"
+    N, nev, nex = 700, 40, 20
+    M = make_matrix("uniform", N, "r2" if real else "g2", seed=12)
+    H = M.dense()
+    ch = pkg.Chase(N, nev, nex, dtype=dtype)
+    ch.set_option("oz_gemm_min", 0)
+    vals, vecs, rep, st = ch.solve(_dev(H), nev, nex, deg=20, tol=1e-10)
+    assert st == 0
+    normH = np.max(np.abs(M.lam))
+    assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
+    ov, _, _ = oracle.chase_solve(H, nev, nex, deg=20, tol=1e-10)
+    assert np.max(np.abs(vals - ov)) <= 1e-10 * normH
+    V = vecs.cpu().numpy()[:, :nev]
+    assert np.max(np.linalg.norm(H @ V - V * vals[None, :], axis=0)) <= 1e-10 * normH
+    assert np.max(np.abs(V.conj().T @ V - np.eye(nev))) <= 1e-12
