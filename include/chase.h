@@ -128,9 +128,10 @@ chase_status chase_init(chase_handle** out, const chase_init_args* args);
  * fp64_emulation=7 (CHASE_C128 / CHASE_R64: the filter's H products run on the INT8 tensor cores
  * as an Ozaki-scheme emulation of FP64 with this many 7-bit slices, 1..7, exact int32 sums,
  * error ~2^-49 ||H|| ||X|| per product; 0 selects the FP64 DMMA kernels and
- * the fused f1 epilogue), oz_gemm_min=4e9 (with the emulation on, the plain GEMMs of the
- * iteration -- CGS against the locked block, the CholQR Gram, Rayleigh-Ritz Q^H (HQ), Q Z,
- * (HQ) Z -- whose M N K reaches this also run on it; a larger value keeps them on DMMA).
+ * the fused f1 epilogue), oz_gemm_min=4e9 and oz_gemm_kmin=12288 (with the emulation on, the
+ * plain GEMMs of the iteration -- the CGS projection against the locked block, the CholQR Gram,
+ * Rayleigh-Ritz Q^H (HQ), Q Z, (HQ) Z -- whose M N K and contraction length K reach these also
+ * run on it; short-K products are faster on DMMA, each emulated launch rewrites the FP64 result).
  * Complex-double grids fall back from the fused reduction to ncclAllReduce when a step would have
  * more tiles than the 2^17 arrival counters per communicator. */
 chase_status chase_set_option(chase_handle* h, const char* key, double value);

@@ -159,7 +159,7 @@ class Chase:
     def set_option(self, key, value):
         """chase_set_option (include/chase.h): deg_max, deg_extra, max_iter (0 = auto), stall_iter, lanczos_steps,
         lanczos_runs, seed_v, seed_lanczos, largest, approx, gemm3m, mixed_filter (f4),
-        fused_reduce / fused_reduce_c64 (f1), peer_timeout, comm_timeout, fp64_emulation, oz_gemm_min."""
+        fused_reduce / fused_reduce_c64 (f1), peer_timeout, comm_timeout, fp64_emulation, oz_gemm_min, oz_gemm_kmin."""
         self._check(self.lib.chase_set_option(self._h, key.encode(), float(value)))
 
     def local_layout(self):

@@ -28,12 +28,15 @@ void allreduce_doubles(chase_handle* h, const Comm& comm, double* x, size_t n) {
   comm_allreduce(comm, x, (int64_t)n, (int64_t)n, 1, DT::F64, Op::Sum, h->stream);
 }
 
-// complex (3M / 4M) or real GEMM by the handle's dtype.  Large plain products of the iteration
-// (RR's Q^H (HQ), Q Z, (HQ) Z; the CholQR Gram; CGS against the locked block) run on the INT8
-// emulation as well when it is on; triangular products (V R^-1) and small ones stay on DMMA.
+// complex (3M / 4M) or real GEMM by the handle's dtype.  Large long-K plain products of the
+// iteration (RR's Q^H (HQ), the CholQR Gram, the CGS projection Y^H V) run on the INT8 emulation as
+// well when it is on; triangular products (V R^-1), short-K and small ones stay on DMMA.
 void gemm(chase_handle* h, const ZgemmDesc& d) {
   if (!h->c64() && h->opt.fp64_emulation > 0 && !h->oz_off && !d.red && !d.S && !d.b_upper &&
-      (double)d.M * d.N * d.K >= h->opt.oz_gemm_min && d.K <= 133143) {
+      (double)d.M * d.N * d.K >= h->opt.oz_gemm_min && d.K >= h->opt.oz_gemm_kmin && d.K <= 133143) {
+    // K >= oz_gemm_kmin (12288): each of the 7 slice-product launches per real product read-modify-writes the
+    // M x N FP64 accumulator once, a cost the MMAs hide only for long K (measured at 30000 x 3000:
+    // Q Z with K = 3000 57 ms emulated vs 25 ms DMMA; the Gram with K = 30000 23 ms vs 37 ms)
     try {
       ozaki_gemm(h, d);
       return;
@@ -566,6 +569,7 @@ chase_status chase_set_option(chase_handle* h, const char* key, double v) {
     if (!key) throw UsageError("null option key");
     std::string k(key);
     if (k == "deg_max") { if (v < 2) throw UsageError("deg_max >= 2"); h->opt.deg_max = (int)v; }
+    else if (k == "oz_gemm_kmin") { if (v < 0) throw UsageError("oz_gemm_kmin >= 0"); h->opt.oz_gemm_kmin = v; }
     else if (k == "oz_gemm_min") { if (v < 0) throw UsageError("oz_gemm_min >= 0"); h->opt.oz_gemm_min = v; }
     else if (k == "deg_extra") { if (v < 0) throw UsageError("deg_extra >= 0"); h->opt.deg_extra = (int)v; }
     else if (k == "max_iter") { if (v < 0) throw UsageError("max_iter >= 0 (0 = auto)"); h->opt.max_iter = (int)v; }

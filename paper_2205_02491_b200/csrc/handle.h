@@ -81,6 +81,7 @@ struct Options {
   double peer_timeout = 120.0;    // f1: seconds a rank waits for its peers' tiles before failing
   double comm_timeout = 0.0;      // host waits poll ncclCommGetAsyncError; > 0: also fail after this many s
   double oz_gemm_min = 4e9;       // plain iteration GEMMs with M N K >= this also run on the emulation
+  double oz_gemm_kmin = 12288;    // ... if their contraction length K is at least this
   int fp64_emulation = 7;         // f4: > 0 = complex-double filter products on INT8 tensor cores (Ozaki, S slices)
 };
 

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(SUB_T) k_sub_eig(const double2* A, int np, con
   }
 }
 
-// ---- 64x64x64 complex tile products on the FP64 tensor cores (DMMA.8x8x4, complex 4M) ------
+// ---- 64x64x64 complex tile products on the FP64 tensor cores (DMMA.8x8x4, complex 3M) ------
 // Tiles live in shared memory in the same swizzled "[k-chunk][row][8 k]" layout the filter GEMM
 // uses (16-byte complex elements, chunk index XOR row%8), so every fragment load of the 8 warps is
 // bank-conflict free.  off(r, k): byte offset of element (row r, contraction index k).
@@ -263,37 +263,55 @@ __device__ __forceinline__ double2 lds_j(uint32_t addr) {
 
 // acc = op(X) * Y with X (rows x k) and Y (k x cols) tiles; warp w owns rows 32*(w/4) + [0,32),
 // cols 16*(w%4) + [0,16): acc[mt][nt][{re,im}][j] = C[32 wm + 8 mt + g][16 wn + 8 nt + 2 t + j].
+// 3M complex product (3 real DMMAs per complex multiply-add, as the filter's zgemm3m):
+// T1 = Xr Yr, T2 = Xi Yi, T3 = (Xr + Xi)(Yr + Yi); Re = T1 - T2, Im = T3 - T1 - T2.
 template <bool CONJX>
 __device__ __forceinline__ void tile_dmma(uint32_t xs, uint32_t ys, double (&acc)[4][2][2][2]) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = w >> 2, wn = w & 3, g = lane >> 2, t = lane & 3;
+  double t3[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+    for (int j = 0; j < 2; ++j) {
+      acc[i][j][0][0] = acc[i][j][0][1] = acc[i][j][1][0] = acc[i][j][1][1] = 0.0;
+      t3[i][j][0] = t3[i][j][1] = 0.0;
+    }
 #pragma unroll 4
   for (int ks = 0; ks < S / 4; ++ks) {
     const int k = (ks >> 1) * 8 + 2 * t + (ks & 1);
     double2 a[4], b[2];
+    double as[4], bs[2];
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
       a[mt] = lds_j(xs + toff(wm * 32 + mt * 8 + g, k));
       if (CONJX) a[mt].y = -a[mt].y;
+      as[mt] = a[mt].x + a[mt].y;
     }
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) b[nt] = lds_j(ys + toff(wn * 16 + nt * 8 + g, k));
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
-      const double nbi = -b[nt].y;
+      b[nt] = lds_j(ys + toff(wn * 16 + nt * 8 + g, k));
+      bs[nt] = b[nt].x + b[nt].y;
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        dmma_j(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].x, b[nt].x);
-        dmma_j(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].x, b[nt].y);
-        dmma_j(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].y, nbi);
-        dmma_j(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].y, b[nt].x);
+        dmma_j(acc[mt][nt][0][0], acc[mt][nt][0][1], a[mt].x, b[nt].x);      // T1
+        dmma_j(acc[mt][nt][1][0], acc[mt][nt][1][1], a[mt].y, b[nt].y);      // T2
+        dmma_j(t3[mt][nt][0], t3[mt][nt][1], as[mt], bs[nt]);                // T3
       }
-    }
   }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double t1 = acc[i][j][0][e], t2 = acc[i][j][1][e];
+        acc[i][j][0][e] = t1 - t2;
+        acc[i][j][1][e] = t3[i][j][e] - t1 - t2;
+      }
 }
 
 __device__ void apply_z_block(double2* Z, int np, const int* pairs, const double2* U, int rt, int k,

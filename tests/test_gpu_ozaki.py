@@ -180,7 +180,7 @@ def test_emulated_step_graded_matrix(direction):
 
 @pytest.mark.parametrize("dtype", ["c128", "r64"])
 def test_iteration_gemms_on_the_emulation(dtype):
-    """oz_gemm_min = 0 routes every plain GEMM of the iteration (CGS, Gram, RR's Q^H (HQ), Q Z,
+    """oz_gemm_min = oz_gemm_kmin = 0 routes every plain GEMM of the iteration (CGS, Gram, RR's Q^H (HQ), Q Z,
     (HQ) Z) through the INT8 emulation too (only V R^-1 stays on DMMA): the solve keeps the
     complex-double bars against the exact spectrum and the oracle."""
     import paper_2205_02491_b200 as pkg
@@ -190,6 +190,7 @@ def test_iteration_gemms_on_the_emulation(dtype):
     H = M.dense()
     ch = pkg.Chase(N, nev, nex, dtype=dtype)
     ch.set_option("oz_gemm_min", 0)
+    ch.set_option("oz_gemm_kmin", 0)
     vals, vecs, rep, st = ch.solve(_dev(H), nev, nex, deg=20, tol=1e-10)
     assert st == 0
     normH = np.max(np.abs(M.lam))
