@@ -1,6 +1,6 @@
 // Cholesky (G = R^H R, R upper) and upper-triangular inverse on the device, blocked with
 // NB = 64: diagonal blocks in one CTA (shared memory), panels by substitution, trailing updates
-// and off-diagonal inverse blocks through the DMMA GEMM (zgemm).  Used by CholQR2 (SURVEY §8
+// through the DMMA GEMM (zgemm); the inverse recursively (half-size off-diagonal blocks).  Used by CholQR2 (SURVEY §8
 // row a7: "Gram -> Cholesky -> V <- V R^-1").
 #include <algorithm>
 #include "common.cuh"
@@ -165,6 +165,33 @@ bool cholesky_upper(void* Gv, int64_t ld, int n, int* d_info, cudaStream_t st) {
   return info == 0;
 }
 
+namespace {
+// X = R^-1 on the leading n x n block, recursively (the diagonal NB-blocks of X are already
+// inverted): X11 = R11^-1, X22 = R22^-1, X12 = -(X11 R12) X22.  Every level is two GEMMs over
+// half-size blocks, so the products stay large (the column-by-column blocked form runs 2(n/NB)
+// GEMMs of at most n x NB outputs -- 1..23 CTAs each at n = 3000).  T: >= n1 n2 scratch.
+void trinv_rec(const double2* R, int64_t ldr, double2* X, int64_t ldx, double2* T, int n, cudaStream_t st) {
+  if (n <= NB) return;
+  const int n1 = ceil_div(ceil_div(n, NB), 2) * NB;       // a multiple of NB
+  const int n2 = n - n1;
+  trinv_rec(R, ldr, X, ldx, T, n1, st);
+  trinv_rec(R + n1 + (int64_t)n1 * ldr, ldr, X + n1 + (int64_t)n1 * ldx, ldx, T, n2, st);
+  ZgemmDesc d;                                             // T = X11 R12   (n1 x n2)
+  d.M = n1; d.N = n2; d.K = n1;
+  d.A = X; d.lda = ldx;
+  d.B = R + (int64_t)n1 * ldr; d.ldb = ldr;
+  d.C = T; d.ldc = n1;
+  zgemm(d, st);
+  ZgemmDesc e;                                             // X12 = -T X22
+  e.M = n1; e.N = n2; e.K = n2;
+  e.A = T; e.lda = n1;
+  e.B = X + n1 + (int64_t)n1 * ldx; e.ldb = ldx;
+  e.C = X + (int64_t)n1 * ldx; e.ldc = ldx;
+  e.alpha = -1.0; e.beta = 0.0;
+  zgemm(e, st);
+}
+}  // namespace
+
 void trinv_upper(const void* Rv, int64_t ldr, void* Xv, int64_t ldx, void* T, int n, cudaStream_t st) {
   const double2* R = reinterpret_cast<const double2*>(Rv);
   double2* X = reinterpret_cast<double2*>(Xv);
@@ -178,25 +205,7 @@ void trinv_upper(const void* Rv, int64_t ldr, void* Xv, int64_t ldx, void* T, in
   }
   k_trinv_diag<<<nblk, NB, smem, st>>>(R, ldr, X, ldx, n);
   CHASE_CHECK_LAUNCH();
-  for (int kb = NB; kb < n; kb += NB) {
-    const int nb = std::min(NB, n - kb);
-    // T = X[0:kb, 0:kb] * R[0:kb, kb:kb+nb]
-    ZgemmDesc d;
-    d.M = kb; d.N = nb; d.K = kb;
-    d.A = X; d.lda = ldx;
-    d.B = R + (int64_t)kb * ldr; d.ldb = ldr;
-    d.C = T; d.ldc = kb;
-    d.alpha = 1.0; d.beta = 0.0;
-    zgemm(d, st);
-    // X[0:kb, kb:kb+nb] = -T * X[kb:kb+nb, kb:kb+nb]
-    ZgemmDesc e;
-    e.M = kb; e.N = nb; e.K = nb;
-    e.A = T; e.lda = kb;
-    e.B = X + kb + (int64_t)kb * ldx; e.ldb = ldx;
-    e.C = X + (int64_t)kb * ldx; e.ldc = ldx;
-    e.alpha = -1.0; e.beta = 0.0;
-    zgemm(e, st);
-  }
+  trinv_rec(R, ldr, X, ldx, reinterpret_cast<double2*>(T), n, st);
 }
 
 }  // namespace chase

@@ -11,7 +11,7 @@ namespace chase {
 bool cholesky_upper(void* G, int64_t ld, int n, int* d_info, cudaStream_t st);
 
 // X = R^{-1} for upper-triangular R (n x n); X (ldx) gets zeros below the diagonal.
-// T: device scratch of >= n * 64 complex.
+// T: device scratch of >= n * n / 4 complex (the recursion's largest off-diagonal block).
 void trinv_upper(const void* R, int64_t ldr, void* X, int64_t ldx, void* T, int n, cudaStream_t st);
 
 // Hermitian eigendecomposition G = Z diag(theta) Z^H by block-cyclic two-sided Jacobi

@@ -85,7 +85,7 @@ bool chol_and_inverse<double>(void* G, void* G2, void* Z, int n, int* d_info, cu
   double2* Gc = reinterpret_cast<double2*>(G2);
   real_to_complex(Gc, n, reinterpret_cast<const double*>(G), n, n, n, st);
   if (!cholesky_upper(Gc, n, n, d_info, st)) return false;
-  trinv_upper(Gc, n, Z, n, G, n, st);                          // G reused as scratch (n x 64 complex)
+  trinv_upper(Gc, n, Z, n, G, n, st);                          // G reused as scratch (n^2/2 complex)
   complex_to_real(reinterpret_cast<double*>(G), n, reinterpret_cast<const double2*>(Z), n, n, n, st);
   *Rinv = G;
   return true;

@@ -184,3 +184,17 @@ def test_solve_from_host_buffers(lib, pinned):
     assert st == 0
     assert np.array_equal(vals_h, vals_d) and rep_h["iterations"] == rep_d["iterations"]
     assert np.array_equal(vh.numpy(), vec_d.cpu().numpy()[:, :nev])
+
+
+@pytest.mark.parametrize("dtype", ["c128", "r64"])
+def test_solve_wide_block(lib, dtype):
+    """nev + nex = 328 (six 64-blocks and a ragged tail): the recursive triangular inverse of
+    CholQR, the block-Jacobi Rayleigh-Ritz and locking at a block width the small cases do not
+    reach, against the exact spectrum."""
+    N, nev, nex = 1400, 220, 108
+    M = make_matrix("uniform", N, "r2" if dtype == "r64" else "g2", seed=21)
+    H = M.dense()
+    ch = lib.Chase(N, nev, nex, dtype=dtype)
+    vals, dvecs, rep, st = ch.solve(_dev(H), nev, nex, deg=20, tol=1e-10)
+    assert st == 0, ch.last_error()
+    _check(M, H, vals, dvecs.cpu().numpy()[:, :nev], nev)
