@@ -32,17 +32,23 @@ void allreduce_doubles(chase_handle* h, const Comm& comm, double* x, size_t n) {
 // iteration (RR's Q^H (HQ), the CholQR Gram, the CGS projection Y^H V) run on the INT8 emulation as
 // well when it is on; triangular products (V R^-1), short-K and small ones stay on DMMA.
 void gemm(chase_handle* h, const ZgemmDesc& d) {
-  if (!h->c64() && h->opt.fp64_emulation > 0 && !h->oz_off && !d.red && !d.S && !d.b_upper &&
+  if (!h->c64() && h->opt.fp64_emulation > 0 && !h->oz_off && !h->oz_gemm_off && !d.red && !d.S && !d.b_upper &&
       (double)d.M * d.N * d.K >= h->opt.oz_gemm_min && d.K >= h->opt.oz_gemm_kmin && d.K <= 133143) {
-    // K >= oz_gemm_kmin (12288): each of the 7 slice-product launches per real product read-modify-writes the
-    // M x N FP64 accumulator once, a cost the MMAs hide only for long K (measured at 30000 x 3000:
-    // Q Z with K = 3000 57 ms emulated vs 25 ms DMMA; the Gram with K = 30000 23 ms vs 37 ms)
+    // K >= oz_gemm_kmin (12288): each of the 7 slice-product launches per real product
+    // read-modify-writes the M x N FP64 accumulator once, a cost the MMAs hide only for long K
+    // (measured at 30000 x 3000: Q Z with K = 3000 57 ms emulated vs 25 ms DMMA; the Gram with
+    // K = 30000 23 ms vs 37 ms)
     try {
       ozaki_gemm(h, d);
       return;
     } catch (const std::bad_alloc&) {
-      h->oz_off = true;
-      ozaki_release(h);
+      // the A operand's slices did not fit: plain GEMMs go back to DMMA, the filter keeps its
+      // emulation (ozaki_gemm allocates before it launches anything)
+      h->oz_gemm_off = true;
+      h->oz_g.slices.release();
+      h->oz_g.exps.release();
+      h->oz_g.diag.release();
+      h->oz_g.src = nullptr;
     }
   }
   if (h->real()) dgemm(d, h->stream);

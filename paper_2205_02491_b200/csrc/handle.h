@@ -115,6 +115,7 @@ struct chase_handle {
     chase::DBuf slices, exps, diag;
   } oz_fwd, oz_g;                     // the shard's set; the A operand of a general emulated GEMM
   bool oz_off = false;                 // fp64_emulation fell back to DMMA (slices did not fit)
+  bool oz_gemm_off = false;            // plain GEMMs back on DMMA (their A slices did not fit)
   chase::DBuf oz_b, oz_t, oz_sync;     // fp64_emulation: slices of the block X, FP64 product accumulators
   const void* h32_src = nullptr;
   int64_t h32_ld = 0;
