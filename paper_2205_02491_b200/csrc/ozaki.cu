@@ -74,6 +74,7 @@ struct Params {
   int amn;                             // 1: A is MN-major (slices [k][m], m contiguous: the forward step)
   int dbg;                             // experiments only (CHASE_OZ_DBG): 1 = drain without the FP64 RMW,
                                        // 2 = every k block re-loads k block 0 (no HBM streaming)
+  int snake;                           // 1: odd rounds walk K backwards (B's last k windows still in L2)
 };
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {   // K-major, SWIZZLE_128B, 8-row groups 1 KB apart
@@ -238,7 +239,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tile_mn(r, tmi, tni);
         const int m0 = tmi * 2 * BM + (int)rank * BM;
         const int nh = tni * BNT + (int)rank * (BN / 2);      // this CTA's half of sub-tile 0
-        for (int kt = 0; kt < KT; ++kt) {
+        // Boustrophedon K order: every round streams all of B's k windows (B does not fit L2), so
+        // odd rounds walk K backwards and start on the windows the previous round read last, which
+        // L2 still holds.  The int32 sums are exact, so the order never changes a result bit.
+        const bool back = p.snake && grouped && (r & 1);
+        for (int kt0 = 0; kt0 < KT; ++kt0) {
+          const int kt = back ? KT - 1 - kt0 : kt0;
           for (int q = 0; q < p.npairs; ++q, ++it) {
             const int s = it % STAGES;
             if (it >= STAGES) mbar_wait(empty + s, ((it / STAGES) - 1) & 1);
@@ -735,6 +741,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d, bool shard) {
   static const int hint_env = [] { const char* e = std::getenv("CHASE_OZ_HINT"); return e ? std::atoi(e) : 0; }();
   static const int dbg_env = [] { const char* e = std::getenv("CHASE_OZ_DBG"); return e ? std::atoi(e) : 0; }();
   static const int sync_env = [] { const char* e = std::getenv("CHASE_OZ_SYNC"); return e ? std::atoi(e) : 1; }();
+  static const int snake_env = [] { const char* e = std::getenv("CHASE_OZ_SNAKE"); return e ? std::atoi(e) : 1; }();
   h->oz_sync.alloc(256);
   if (16129LL * K > 2147483647LL) throw UsageError("fp64_emulation: K > 133143 needs K chunking (not built)");
   const int ptiles = ceil_div(M, 2 * oz::BM) * ceil_div(N, ns * oz::BN);
@@ -781,6 +788,7 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d, bool shard) {
         prm.hint = hint_env;
         prm.amn = dir == 0 ? 1 : 0;
         prm.dbg = dbg_env;
+        prm.snake = snake_env;
         prm.sync = nullptr;
         if (sync_env && !h->colocated) {     // co-located ranks share the SMs: no round barrier
           CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, st));
