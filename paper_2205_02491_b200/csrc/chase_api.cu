@@ -428,7 +428,7 @@ chase_status chase_nccl_unique_id(void* out128) {
 }
 
 const char* chase_version(void) {
-  return "chase-b200 0.2 (sm_100a: FP64 DMMA + TMA filter, tcgen05 3xTF32 complex single, fused NVLink all-reduce)";
+  return "chase-b200 0.3 (sm_100a: FP64 via Ozaki INT8 tcgen05 emulation or DMMA, tcgen05 3xTF32 complex single, NCCL / fused NVLink all-reduce)";
 }
 
 const char* chase_last_error(const chase_handle* h) { return h ? h->err.c_str() : "null handle"; }
