@@ -431,24 +431,32 @@ def main():
     achieved = flops / world / filt_s_max / 1e12
     dmma_peak, tf32_peak, i8_peak, peak_src = load_peaks()
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r02_ncu_ozaki_step.json" if EMU else "r01_ncu_filter_gemm.json")
+    scheme = int(ch.get_option("ozaki_scheme")) if EMU else 0     # 2 = CRT (scheme II), 1 = slices
+    prof = os.path.join(ROOT, "profiles", {2: "r02_ncu_ozaki_crt_step.json", 1: "r02_ncu_ozaki_step.json"}.get(
+        scheme, "r01_ncu_filter_gemm.json"))
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_step" if EMU else "dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("dram_bytes_per_step" if scheme else "dram_bytes_per_launch")
         except Exception:
             traffic = None
-    if EMU:
-        # a complex MAC costs 3 real products (3M) x S(S+1)/2 slice products = 84 int8 MACs (168 ops)
-        # for 8 algorithmic flop: the emulation's ceiling is the INT8 tensor peak x 8 / 168
-        pairs = EMU * (EMU + 1) // 2
-        peak_c = i8_peak * 8.0 / (2.0 * 3 * pairs)
+
+    def emu_peak(sch):
+        # int8 GEMMs per complex MAC: 3 real products (3M) x 16 moduli (scheme II) or x S(S+1)/2
+        # slice pairs (S = 7: 28); 2 int8 ops per int8 MAC, 8 algorithmic flop per complex MAC
+        prods = 16 if sch == 2 else EMU * (EMU + 1) // 2
+        return i8_peak * 8.0 / (2.0 * 3 * prods), 2 * 3 * prods
+
+    if scheme:
+        peak_c, ops = emu_peak(scheme)
+        what = ("Ozaki scheme II: residues of the 52-bit scaled operands modulo 16 coprime moduli, one int8 GEMM "
+                "per modulus, exact CRT reconstruction" if scheme == 2 else f"Ozaki scheme, {EMU} slices")
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak_c, "unit": "TFLOP/s", "frac": achieved / peak_c,
                 "traffic": traffic,
-                "kernel": "oz_gemm_kernel (filter step: FP64 complex product emulated on INT8 tcgen05 MMAs, Ozaki "
-                          f"scheme, {EMU} slices, 3M; + slicing / recombination kernels, all inside the timed filter phase)",
+                "kernel": "oz_gemm_kernel (filter step: FP64 complex product emulated on INT8 tcgen05 MMAs, "
+                          f"{what}, 3M; + residue / reconstruction kernels, all inside the timed filter phase)",
                 "per_launch_flops": per_launch_flops, "launches": launches_filter, "unit_of_launch": "one fused filter step",
                 "int8_pipe_frac": achieved / peak_c,
-                "peak_source": f"INT8 tcgen05 peak {i8_peak:.0f} TOPS ({peak_src}) x 8 / {2 * 3 * pairs} "
+                "peak_source": f"INT8 tcgen05 peak {i8_peak:.0f} TOPS ({peak_src}) x 8 / {ops} "
                                "(int8 ops per algorithmic complex flop)"}
     else:
         roof = {"bound": "tensor", "achieved": achieved, "peak": dmma_peak * 4.0 / 3.0, "unit": "TFLOP/s",
@@ -530,11 +538,15 @@ def main():
         ch3.solve(H3, nev3, nex3, deg=DEG, tol=1e-10, vectors=v3)
         _, _, r3, _ = ch3.solve(H3, nev3, nex3, deg=DEG, tol=1e-10, vectors=v3)
         f3 = 8.0 * N3 * N3 * r3["matvecs"]
+        scheme3 = int(ch3.get_option("ozaki_scheme")) if EMU else 0
+        peak3 = emu_peak(scheme3)[0] if scheme3 else dmma_peak * 4.0 / 3.0
         cfg3 = {"workload": f"config3: N={N3} complex double geometric, nev={nev3}, nex={nex3}, deg={DEG}, one subspace "
                             "iteration (P:727-731), 1x1; 1 warm-up + 1 timed iteration; same product path as the main line",
                 "value": f3 / r3["t_all"] / 1e12, "unit": "TFLOP/s", "ms_per_step": r3["t_all"] * 1e3,
                 "filter_tflops": f3 / r3["t_filter"] / 1e12,
-                "roofline_frac": f3 / r3["t_filter"] / 1e12 / roof["peak"],
+                "roofline_frac": f3 / r3["t_filter"] / 1e12 / peak3,
+                "fp64_products": {0: "FP64 DMMA", 1: "Ozaki slices (the residues of the 57.6 GB shard do not fit)",
+                                  2: "Ozaki scheme II"}[scheme3],
                 "phases_s": {k: r3[k] for k in ("t_lanczos", "t_filter", "t_qr", "t_rr", "t_resid", "t_all")}}
         ch3.close()
         del H3, v3
@@ -547,7 +559,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": dev_s_max / args.steps * 1e3,
                 "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-                "dtype": "c128 (products: int8 slices -> int32 -> f64)" if EMU else "c128",
+                "dtype": ("c128 (products: int8 residues -> int32 -> exact CRT -> f64)" if scheme == 2 else
+                          "c128 (products: int8 slices -> int32 -> f64)" if scheme == 1 else "c128"),
                 "data": f"synthetic (seeded G2 generator: H = Phi P C P^H Phi^H with the Table 1 {args.family} spectrum, d_max=1, eps=1e-4)",
                 "config": {"workload": ({(N1, NEV, NEX): "config2", (60000, 1000, 300): "config3",
                                          (115000, 1200, 400): "config4"}.get((args.n, nev, nex), "custom")
@@ -559,8 +572,10 @@ def main():
                 "phases_s_per_step": phases,
                 "filter_tflops_per_gpu": achieved,
                 "roofline": roof,
-                "fp64_products": ("Ozaki-scheme emulation on INT8 tensor cores (7 slices, step error ~1e-14 vs FP64 "
-                                  "DMMA; SURVEY f4)" if EMU else "FP64 DMMA"),
+                "fp64_products": {2: "Ozaki scheme II on INT8 tensor cores (16 CRT moduli, exact integer products, one "
+                                     "FP64 rounding; step error ~9e-15 vs FP64 DMMA; SURVEY f4)",
+                                  1: "Ozaki-scheme emulation on INT8 tensor cores (7 slices, step error ~1e-14 vs FP64 "
+                                     "DMMA; SURVEY f4)", 0: "FP64 DMMA"}[scheme],
                 "clocks": clocks, "gpu_launches": launches, "e2e": e2e}
         if other:
             line["c128_dmma_iteration" if EMU else "c128_ozaki_iteration"] = other

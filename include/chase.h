@@ -126,15 +126,24 @@ chase_status chase_init(chase_handle** out, const chase_init_args* args);
  * comm_timeout=0 (host waits poll ncclCommGetAsyncError; a value > 0 also fails a wait that
  * exceeds it, e.g. when a peer died -- its communicators are aborted on CUDA/NCCL errors),
  * fp64_emulation=7 (CHASE_C128 / CHASE_R64: the filter's H products run on the INT8 tensor cores
- * as an Ozaki-scheme emulation of FP64 with this many 7-bit slices, 1..7, exact int32 sums,
- * error ~2^-49 ||H|| ||X|| per product; 0 selects the FP64 DMMA kernels and
- * the fused f1 epilogue), oz_gemm_min=4e9 and oz_gemm_kmin=12288 (with the emulation on, the
+ * as an Ozaki-scheme emulation of FP64 with exact int32 sums; 0 selects the
+ * FP64 DMMA kernels and the fused f1 epilogue), oz_crt=1 (scheme II: the 52-bit scaled operands'
+ * residues modulo 16 coprime moduli, 16 int8 GEMMs per real product and an exact Chinese-
+ * remainder reconstruction -- one FP64 rounding per product; 48 B of residues per complex
+ * element of H; when they do not fit, or with oz_crt=0, the slice scheme: fp64_emulation 7-bit
+ * slices, 3..8, 28 int8 GEMMs per real product at 7, error ~2^-49 ||H|| ||X||, 21 B per element), oz_gemm_min=4e9 and oz_gemm_kmin=12288 (with the emulation on, the
  * plain GEMMs of the iteration -- the CGS projection against the locked block, the CholQR Gram,
  * Rayleigh-Ritz Q^H (HQ), Q Z, (HQ) Z -- whose M N K and contraction length K reach these also
  * run on it; short-K products are faster on DMMA, each emulated launch rewrites the FP64 result).
  * Complex-double grids fall back from the fused reduction to ncclAllReduce when a step would have
  * more tiles than the 2^17 arrival counters per communicator. */
 chase_status chase_set_option(chase_handle* h, const char* key, double value);
+
+/* Read an option or the path in effect: key "ozaki_scheme" -> 0 (FP64 DMMA products: emulation
+ * off, complex single, or no room for it), 1 (7-slice Ozaki scheme), 2 (Ozaki scheme II, CRT);
+ * also oz_crt, fp64_emulation, deg_max, deg_extra, max_iter, mixed_filter (the current values,
+ * after any fallback).  *value is written on CHASE_OK; unknown key -> CHASE_E_USAGE.  Local. */
+chase_status chase_get_option(chase_handle* h, const char* key, double* value);
 
 /* This rank's shard: rows [row0, row0+p) and columns [col0, col0+q) of H. */
 chase_status chase_local_layout(const chase_handle* h, int64_t* row0, int64_t* p, int64_t* col0,

@@ -17,7 +17,7 @@ STATUS_NAMES = {0: "CHASE_OK", 2: "CHASE_E_USAGE", 3: "CHASE_E_NUMERIC", 4: "CHA
                 5: "CHASE_E_CUDA", 6: "CHASE_E_NCCL", 7: "CHASE_E_NOMEM", 8: "CHASE_E_MAXITER"}
 
 # exported symbols (include/chase.h); tests check that every one is present
-EXPORTS = ("chase_init", "chase_set_option", "chase_local_layout", "chase_solve", "chase_hemm_step",
+EXPORTS = ("chase_init", "chase_set_option", "chase_get_option", "chase_local_layout", "chase_solve", "chase_hemm_step",
            "chase_filter", "chase_lanczos", "chase_random_block", "chase_finalize",
            "chase_last_error", "chase_version", "chase_nccl_unique_id", "chase_kernel_launches", "chase_heev")
 
@@ -61,6 +61,7 @@ def load():
     P = C.POINTER
     lib.chase_init.argtypes = [P(vp), P(InitArgs)]
     lib.chase_set_option.argtypes = [vp, C.c_char_p, dbl]
+    lib.chase_get_option.argtypes = [vp, C.c_char_p, C.POINTER(dbl)]
     lib.chase_local_layout.argtypes = [vp, P(i64), P(i64), P(i64), P(i64)]
     lib.chase_solve.argtypes = [vp, vp, i64, i64, i32, i32, i32, dbl, P(dbl), vp, i64, P(Report)]
     lib.chase_hemm_step.argtypes = [vp, i32, vp, i64, vp, i64, vp, i64, i32, dbl, dbl, dbl]
@@ -161,6 +162,12 @@ class Chase:
         lanczos_runs, seed_v, seed_lanczos, largest, approx, gemm3m, mixed_filter (f4),
         fused_reduce / fused_reduce_c64 (f1), peer_timeout, comm_timeout, fp64_emulation, oz_gemm_min, oz_gemm_kmin."""
         self._check(self.lib.chase_set_option(self._h, key.encode(), float(value)))
+
+    def get_option(self, key):
+        """chase_get_option: an option's current value, or "ozaki_scheme" (0 DMMA, 1 slices, 2 CRT)."""
+        v = C.c_double()
+        self._check(self.lib.chase_get_option(self._h, key.encode(), C.byref(v)))
+        return v.value
 
     def local_layout(self):
         r0, p, c0, q = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()

@@ -33,7 +33,8 @@ void allreduce_doubles(chase_handle* h, const Comm& comm, double* x, size_t n) {
 // well when it is on; triangular products (V R^-1), short-K and small ones stay on DMMA.
 void gemm(chase_handle* h, const ZgemmDesc& d) {
   if (!h->c64() && h->opt.fp64_emulation > 0 && !h->oz_off && !h->oz_gemm_off && !d.red && !d.S && !d.b_upper &&
-      (double)d.M * d.N * d.K >= h->opt.oz_gemm_min && d.K >= h->opt.oz_gemm_kmin && d.K <= 133143) {
+      (double)d.M * d.N * d.K >= h->opt.oz_gemm_min && d.K >= h->opt.oz_gemm_kmin &&
+      d.K <= (h->opt.oz_crt ? 131071 : 133143)) {
     // K >= oz_gemm_kmin (12288): each of the 7 slice-product launches per real product
     // read-modify-writes the M x N FP64 accumulator once, a cost the MMAs hide only for long K
     // (measured at 30000 x 3000: Q Z with K = 3000 57 ms emulated vs 25 ms DMMA; the Gram with
@@ -94,13 +95,24 @@ static ZgemmDesc step_desc(chase_handle* h, int dir, const void* H, int64_t ldh,
 // (default, S = 7).  Falls back to DMMA for good when the slices do not fit in device memory, and
 // for K > 133143 (int32-exact accumulation bound; K chunking is not built).
 static void step_gemm(chase_handle* h, const ZgemmDesc& d) {
-  if (!h->c64() && h->opt.fp64_emulation > 0 && !d.red && !h->oz_off && d.K <= 133143) {
+  if (!h->c64() && h->opt.fp64_emulation > 0 && !d.red && !h->oz_off && d.K <= (h->opt.oz_crt ? 131071 : 133143)) {
     try {
       ozaki_step(h, d);
       return;
     } catch (const std::bad_alloc&) {
-      h->oz_off = true;
+      // (every emulated product allocates before it launches, and only its own buffers are
+      // written before the final combine, so a retry starts clean)
       ozaki_release(h);
+      if (h->opt.oz_crt) {               // scheme II's residues (48 B per element) did not fit:
+        h->opt.oz_crt = 0;               // the 7-slice scheme (21 B per element)
+        try {
+          ozaki_step(h, d);
+          return;
+        } catch (const std::bad_alloc&) {
+          ozaki_release(h);
+        }
+      }
+      h->oz_off = true;
     }
   }
   gemm(h, d);
@@ -570,11 +582,31 @@ chase_status chase_init(chase_handle** out, const chase_init_args* a) {
   return CHASE_OK;
 }
 
+chase_status chase_get_option(chase_handle* h, const char* key, double* value) {
+  return guarded(h, [&]() {
+    if (!key || !value) throw UsageError("null option key or value pointer");
+    std::string k(key);
+    double v;
+    if (k == "ozaki_scheme")             // the FP64 product path in effect (after any memory fallback)
+      v = (h->c64() || h->opt.fp64_emulation <= 0 || h->oz_off) ? 0.0 : (h->opt.oz_crt ? 2.0 : 1.0);
+    else if (k == "oz_crt") v = h->opt.oz_crt;
+    else if (k == "fp64_emulation") v = h->opt.fp64_emulation;
+    else if (k == "deg_max") v = h->opt.deg_max;
+    else if (k == "deg_extra") v = h->opt.deg_extra;
+    else if (k == "max_iter") v = h->opt.max_iter;
+    else if (k == "mixed_filter") v = h->opt.mixed_filter;
+    else throw UsageError("unknown option " + k);
+    *value = v;
+    return CHASE_OK;
+  }, false);
+}
+
 chase_status chase_set_option(chase_handle* h, const char* key, double v) {
   return guarded(h, [&]() {
     if (!key) throw UsageError("null option key");
     std::string k(key);
     if (k == "deg_max") { if (v < 2) throw UsageError("deg_max >= 2"); h->opt.deg_max = (int)v; }
+    else if (k == "oz_crt") { h->opt.oz_crt = v != 0.0 ? 1 : 0; invalidate_shard_caches(h); }
     else if (k == "oz_gemm_kmin") { if (v < 0) throw UsageError("oz_gemm_kmin >= 0"); h->opt.oz_gemm_kmin = v; }
     else if (k == "oz_gemm_min") { if (v < 0) throw UsageError("oz_gemm_min >= 0"); h->opt.oz_gemm_min = v; }
     else if (k == "deg_extra") { if (v < 0) throw UsageError("deg_extra >= 0"); h->opt.deg_extra = (int)v; }

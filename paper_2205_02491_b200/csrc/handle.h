@@ -82,7 +82,8 @@ struct Options {
   double comm_timeout = 0.0;      // host waits poll ncclCommGetAsyncError; > 0: also fail after this many s
   double oz_gemm_min = 4e9;       // plain iteration GEMMs with M N K >= this also run on the emulation
   double oz_gemm_kmin = 12288;    // ... if their contraction length K is at least this
-  int fp64_emulation = 7;         // f4: > 0 = complex-double filter products on INT8 tensor cores (Ozaki, S slices)
+  int fp64_emulation = 7;          // f4: > 0 = complex-double filter products on INT8 tensor cores (Ozaki)
+  int oz_crt = 1;                  // 1: Ozaki scheme II (16 CRT moduli); 0 (or no room for the residues): S slices
 };
 
 }  // namespace chase
@@ -117,6 +118,7 @@ struct chase_handle {
   bool oz_off = false;                 // fp64_emulation fell back to DMMA (slices did not fit)
   bool oz_gemm_off = false;            // plain GEMMs back on DMMA (their A slices did not fit)
   chase::DBuf oz_b, oz_t, oz_sync;     // fp64_emulation: slices of the block X, FP64 product accumulators
+  chase::DBuf oz_i;                    // oz_crt: the products' residues (one byte per modulus and output)
   const void* h32_src = nullptr;
   int64_t h32_ld = 0;
   const void* hlo_src = nullptr;

@@ -75,6 +75,8 @@ struct Params {
   int dbg;                             // experiments only (CHASE_OZ_DBG): 1 = drain without the FP64 RMW,
                                        // 2 = every k block re-loads k block 0 (no HBM streaming)
   int snake;                           // 1: odd rounds walk K backwards (B's last k windows still in L2)
+  uint8_t* rout;                       // CRT mode: the product mod `modulus`, one byte per output (ld ldo)
+  int modulus;
 };
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {   // K-major, SWIZZLE_128B, 8-row groups 1 KB apart
@@ -329,7 +331,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
             : "r"(base + c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (row < p.M && !(p.dbg & 1)) {
+        if (p.rout) {
+          if (row < p.M) {
+            const double m = (double)p.modulus, inv_m = 1.0 / m;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int n = n0 + c0 + j;
+              if (n < p.N) {
+                const double a = (double)(int)r[j];            // exact int32 product
+                double t = fma(-rint(a * inv_m), m, a);        // exact, |t| <= 1.5 m
+                if (t < 0.0) t += m;
+                if (t < 0.0) t += m;
+                if (t >= m) t -= m;
+                p.rout[(int64_t)row + (int64_t)n * p.ldo] = (uint8_t)(int)t;
+              }
+            }
+          }
+        } else if (row < p.M && !(p.dbg & 1)) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int n = n0 + c0 + j;
@@ -377,6 +395,34 @@ __device__ __forceinline__ void cut(double v, int8_t (&a)[S]) {
     const double t = rint(v);
     a[s] = (int8_t)(int)t;
     v -= t;
+  }
+}
+
+// ---- Ozaki scheme II (CRT; option oz_crt): instead of slices, the 52-bit integer
+// A' = rint(v 2^52) of every scaled value (|v| < 1) is stored as its residues modulo 16 pairwise
+// coprime moduli <= 256 (symmetric, |r| <= 128); one int8 GEMM per modulus gives A'B' mod m_i
+// exactly (|r_a r_b| K <= 2^14 K < 2^31 for K <= 131071), and Garner's algorithm rebuilds A'B'
+// (|A'B'| <= K 2^104 < M / 2, M = prod m_i ~ 2^125) exactly before one FP64 rounding.
+constexpr int NMOD = 16;
+__host__ __device__ constexpr int crt_mod(int i) {
+  constexpr int m[NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+  return m[i];
+}
+constexpr int CRT_BITS = 52;
+
+__device__ __forceinline__ void crt_cut(double v, int8_t (&a)[NMOD]) {
+  const double A = rint(v * 4503599627370496.0);          // 2^52 v, |A| < 2^52: exact integer
+#pragma unroll
+  for (int i = 0; i < NMOD; ++i) {
+    const int mi = crt_mod(i);
+    const double m = (double)mi;
+    const double hi = mi == 256 ? 127.0 : 0.5 * (m - 1.0), lo = mi == 256 ? -128.0 : -hi;
+    const double q = rint(A * (1.0 / m));                  // within one of A / m
+    double r = fma(-q, m, A);                              // exact (|q m| < 2^53), |r| <= 1.5 m
+    if (r > hi) r -= m;
+    if (r < lo) r += m;
+    if (r > hi) r -= m;
+    a[i] = (int8_t)(int)r;
   }
 }
 
@@ -451,6 +497,40 @@ __global__ void __launch_bounds__(256) oz_slice_lines(const T* X, int64_t ld, in
   double sc[NP];
 #pragma unroll
   for (int P = 0; P < NP; ++P) sc[P] = ldexp(1.0, -ex[P]);
+  if constexpr (S == NMOD) {
+    // scheme II: the 4 values of a thread loaded once, then one real component at a time (16
+    // residue words live at once instead of 48: occupancy)
+    for (int k4 = threadIdx.x * 4; k4 < (int)ldk; k4 += 256 * 4) {
+      double vv[4][NP];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = k4 + kk;
+        if (k < rows && k != kd) {
+          load(k, vv[kk]);
+        } else {
+#pragma unroll
+          for (int P = 0; P < NP; ++P) vv[kk][P] = 0.0;
+        }
+      }
+      int8_t* o = out + (int64_t)c * ldk + k4;
+#pragma unroll
+      for (int P = 0; P < NP; ++P) {
+        uint32_t packed[NMOD];
+#pragma unroll
+        for (int i = 0; i < NMOD; ++i) packed[i] = 0;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          int8_t a[NMOD];
+          crt_cut(vv[kk][P] * sc[P], a);
+#pragma unroll
+          for (int i = 0; i < NMOD; ++i) packed[i] |= (uint32_t)(uint8_t)a[i] << (8 * kk);
+        }
+#pragma unroll
+        for (int i = 0; i < NMOD; ++i) *reinterpret_cast<uint32_t*>(o + (int64_t)(P * NMOD + i) * plane) = packed[i];
+      }
+    }
+    return;
+  }
   // 4 consecutive k per thread: one 4-byte store per slice (ldk % 128 == 0)
   for (int k4 = threadIdx.x * 4; k4 < (int)ldk; k4 += 256 * 4) {
     uint32_t packed[NP][S];
@@ -470,7 +550,10 @@ __global__ void __launch_bounds__(256) oz_slice_lines(const T* X, int64_t ld, in
       }
       int8_t a[NP][S];
 #pragma unroll
-      for (int P = 0; P < NP; ++P) cut<S>(v[P] * sc[P], a[P]);
+      for (int P = 0; P < NP; ++P) {
+        if constexpr (S == NMOD) crt_cut(v[P] * sc[P], a[P]);   // scheme II: residues
+        else cut<S>(v[P] * sc[P], a[P]);
+      }
 #pragma unroll
       for (int P = 0; P < NP; ++P)
 #pragma unroll
@@ -561,6 +644,75 @@ __global__ void oz_combine(const double* T_, int64_t ldt, int64_t tplane, const 
   }
 }
 
+// Scheme II reconstruction: the NMOD residues of one real product (byte planes of M x N, ld M,
+// written by the GEMM drain) -> Garner's mixed-radix digits (balanced: the representation of
+// A'B' in (-M/2, M/2), exact) -> A'B' by Horner in 128-bit integers -> one rounding to FP64 ->
+// times 2^-104 into T (ld ldt), where oz_combine picks it up like a slice-scheme accumulator.
+__host__ __device__ constexpr int inv_mod(int a, int m) {   // a^-1 mod m (gcd(a, m) = 1)
+  int t = 0, nt = 1, r = m, nr = a % m;
+  while (nr != 0) {
+    const int qq = r / nr;
+    int tmp = t - qq * nt; t = nt; nt = tmp;
+    tmp = r - qq * nr; r = nr; nr = tmp;
+  }
+  return t < 0 ? t + m : t;
+}
+__host__ __device__ constexpr int pmod(int i, int j) {      // (m_0 ... m_{i-1}) mod m_j
+  int p = 1;
+  for (int k = 0; k < i; ++k) p = p * (crt_mod(k) % crt_mod(j)) % crt_mod(j);
+  return p;
+}
+// Garner digit J: v_J = (c_J - sum_{i<J} v_i P_i) P_J^-1 mod m_J (balanced), where
+// R[J] = sum_{i<J} v_i (P_i mod m_J) is accumulated as the digits appear (|R| < 2^19).
+template <int J, int K>
+struct CrtUpd {
+  __device__ __forceinline__ static void run(int vj, int (&R)[NMOD]) {
+    constexpr int pm = pmod(J, K);
+    R[K] += vj * pm;
+    CrtUpd<J, K + 1>::run(vj, R);
+  }
+};
+template <int J>
+struct CrtUpd<J, NMOD> {
+  __device__ __forceinline__ static void run(int, int (&)[NMOD]) {}
+};
+template <int J>
+struct CrtDig {
+  __device__ __forceinline__ static void run(const uint8_t* c, int64_t iplane, int64_t idx, int (&v)[NMOD],
+                                             int (&R)[NMOD]) {
+    constexpr int mj = crt_mod(J);
+    constexpr int invp = inv_mod(pmod(J, J), mj);
+    constexpr int hi = mj == 256 ? 127 : (mj - 1) / 2;
+    int t = ((int)c[(int64_t)J * iplane + idx] - R[J]) % mj;
+    if (t < 0) t += mj;
+    t = (t * invp) % mj;
+    const int vj = t > hi ? t - mj : t;
+    v[J] = vj;
+    CrtUpd<J, J + 1>::run(vj, R);
+    CrtDig<J + 1>::run(c, iplane, idx, v, R);
+  }
+};
+template <>
+struct CrtDig<NMOD> {
+  __device__ __forceinline__ static void run(const uint8_t*, int64_t, int64_t, int (&)[NMOD], int (&)[NMOD]) {}
+};
+
+__global__ void __launch_bounds__(256) oz_crt(const uint8_t* C, int64_t iplane, int M, int N, double* T, int64_t ldt) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    int v[NMOD], R[NMOD];
+#pragma unroll
+    for (int j = 0; j < NMOD; ++j) R[j] = 0;
+    CrtDig<0>::run(C, iplane, idx, v, R);
+    // Horner in 128-bit integers (|A'B'| < 2^124: exact), one rounding to FP64 at the end
+    __int128 x = v[NMOD - 1];
+#pragma unroll
+    for (int j = NMOD - 2; j >= 0; --j) x = x * crt_mod(j) + v[j];
+    const int m = (int)(idx % M), n = (int)(idx / M);
+    T[(int64_t)m + (int64_t)n * ldt] = (double)x * 4.930380657631324e-32;   // 2^-104
+  }
+}
+
 // the diagonal element of output row m (forward: H[m][m + off]; backward: conj(H[m - off][m])),
 // zero where row m does not cross the global diagonal (off = r0 - c0)
 __device__ __forceinline__ double2 as_c(double2 v) { return v; }
@@ -606,7 +758,9 @@ inline int64_t ldk_of(int64_t K) { return (K + 127) / 128 * 128; }   // 16-B TMA
 // ------------------------------------------------------------------------------------ host
 using OzShard = chase_handle::OzShard;    // the shard's slice set (cached on the handle within one API call)
 
-static int oz_slices_opt(chase_handle* h) { return std::min(8, std::max(0, h->opt.fp64_emulation)); }
+static int oz_slices_opt(chase_handle* h) {      // planes per real component: slices, or NMOD residues
+  return h->opt.oz_crt ? oz::NMOD : std::min(8, std::max(0, h->opt.fp64_emulation));
+}
 
 template <int S, class T>
 static void slice_lines(const T* X, int64_t ld, int rows, int lines, int sg3, int diag, const int* kexp, int kexp_ld,
@@ -626,6 +780,7 @@ static void with_S(int S, F&& f) {
     case 6: f(std::integral_constant<int, 6>{}); break;
     case 7: f(std::integral_constant<int, 7>{}); break;
     case 8: f(std::integral_constant<int, 8>{}); break;
+    case oz::NMOD: f(std::integral_constant<int, oz::NMOD>{}); break;
     default: throw UsageError("fp64_emulation: slices must be 3..8");
   }
 }
@@ -646,6 +801,12 @@ static void oz_slice_matrix(chase_handle* h, OzShard& z, const void* H, int64_t 
   constexpr int NP = oz::Comp<T>::NP;
   const int S = oz_slices_opt(h);
   const int64_t ldk = oz::ldk_of(p);
+  if (S == oz::NMOD) {
+    // test hook: a residue set larger than CHASE_OZ_CRT_MAXBYTES behaves as if it did not fit
+    const char* cap_e = std::getenv("CHASE_OZ_CRT_MAXBYTES");
+    const double cap = cap_e ? std::atof(cap_e) : 0.0;
+    if (cap > 0.0 && (double)NP * S * q * ldk > cap) throw std::bad_alloc();
+  }
   z.slices.alloc((size_t)NP * S * q * ldk);
   // exps: r [NP][p] | c [NP][q] | row maxima (u64) [NP][p]
   const size_t ri = (size_t)NP * p, ci = (size_t)NP * q;
@@ -744,6 +905,13 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d, bool shard) {
   static const int snake_env = [] { const char* e = std::getenv("CHASE_OZ_SNAKE"); return e ? std::atoi(e) : 1; }();
   h->oz_sync.alloc(256);
   if (16129LL * K > 2147483647LL) throw UsageError("fp64_emulation: K > 133143 needs K chunking (not built)");
+  const bool crt = S == oz::NMOD;
+  if (crt && 16384LL * K > 2147483647LL) throw UsageError("oz_crt: K > 131071 needs K chunking (not built)");
+  uint8_t* Ibuf = nullptr;
+  if (crt) {
+    h->oz_i.alloc((size_t)oz::NMOD * M * N);
+    Ibuf = h->oz_i.as<uint8_t>();
+  }
   const int ptiles = ceil_div(M, 2 * oz::BM) * ceil_div(N, ns * oz::BN);
   int sms = 148;
   {
@@ -758,6 +926,33 @@ static void ozaki_step_t(chase_handle* h, const ZgemmDesc& d, bool shard) {
     oz::make_slice_tmap(&ta, A.slices.as<int8_t>() + (size_t)P * S * qq * ldka, pp, qq, ldka, S, oz::BM);
     oz::make_slice_tmap(&tb, bsl + (size_t)P * S * N * ldkb, K, N, ldkb, S, oz::BN / 2);
     bool first = true;
+    if (crt) {
+      // scheme II: one launch per modulus (residue plane i of A times plane i of B), then Garner
+      for (int i = 0; i < oz::NMOD; ++i) {
+        oz::Params prm{};
+        prm.M = M; prm.N = N; prm.K = K;
+        prm.npairs = 1;
+        prm.sa[0] = i;
+        prm.tb[0] = i;
+        prm.scale = 1.0;
+        prm.out = nullptr;
+        prm.rout = Ibuf + (size_t)i * M * N;
+        prm.modulus = oz::crt_mod(i);
+        prm.ldo = M;
+        prm.amn = dir == 0 ? 1 : 0;
+        prm.snake = snake_env;
+        prm.sync = nullptr;
+        if (sync_env && !h->colocated) {
+          CHASE_CUDA(cudaMemsetAsync(h->oz_sync.p, 0, 64, st));
+          prm.sync = h->oz_sync.as<unsigned>();
+        }
+        oz::oz_gemm_kernel<1><<<grid, oz::THREADS, oz::Shape<1>::SMEM, st>>>(ta, tb, prm);
+        CHASE_CHECK_LAUNCH();
+      }
+      oz::oz_crt<<<148 * 8, 256, 0, st>>>(Ibuf, (int64_t)M * N, M, N, Tacc + (size_t)P * M * N, M);
+      CHASE_CHECK_LAUNCH();
+      continue;
+    }
     for (int dsum = 2; dsum <= S + 1; ++dsum) {
       std::vector<std::pair<int, int>> pairs;
       for (int s = 1; s < dsum; ++s)
@@ -840,6 +1035,7 @@ void ozaki_release(chase_handle* h) {
   }
   h->oz_b.release();
   h->oz_t.release();
+  h->oz_i.release();
   h->oz_sync.release();
 }
 

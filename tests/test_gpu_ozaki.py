@@ -27,9 +27,10 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
+@pytest.mark.parametrize("crt", [0, 1], ids=["slices", "crt"])
 @pytest.mark.parametrize("direction", [0, 1])
 @pytest.mark.parametrize("N,n", [(600, 37), (777, 300), (130, 1)])
-def test_emulated_product_is_exact_on_representable_inputs(direction, N, n):
+def test_emulated_product_is_exact_on_representable_inputs(direction, N, n, crt):
     import paper_2205_02491_b200 as pkg
     rng = np.random.default_rng(N + n)
     Hr, Hi = rng.integers(-100, 101, (N, N)), rng.integers(-100, 101, (N, N))
@@ -46,14 +47,16 @@ def test_emulated_product_is_exact_on_representable_inputs(direction, N, n):
     ref = (re + 1j * im) * 2.0 ** -13
     ch = pkg.Chase(N, n, 1)
     ch.set_option("fp64_emulation", 7)
+    ch.set_option("oz_crt", crt)
     dY = _dev(np.zeros((N, n), dtype=complex))
     ch.hemm_step(direction, _dev(H), _dev(X), dY, n, 1.0, 0.0, 0.0)
     assert np.array_equal(dY.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("crt", [0, 1], ids=["slices", "crt"])
 @pytest.mark.parametrize("direction", [0, 1])
 @pytest.mark.parametrize("N,n", [(1000, 75), (1300, 257), (333, 7)])
-def test_emulated_step_vs_oracle(direction, N, n):
+def test_emulated_step_vs_oracle(direction, N, n, crt):
     import paper_2205_02491_b200 as pkg
     M = make_matrix("uniform", N, "g2", seed=N)
     H = M.dense()
@@ -63,6 +66,7 @@ def test_emulated_step_vs_oracle(direction, N, n):
     ref = oracle.hemm_step(H, X, Y0, 0.37, -0.81, 0.55)
     ch = pkg.Chase(N, n, 1)
     ch.set_option("fp64_emulation", 7)
+    ch.set_option("oz_crt", crt)
     dY = _dev(Y0)
     ch.hemm_step(direction, _dev(H), _dev(X), dY, n, 0.37, -0.81, 0.55)
     err = _rel(dY.cpu().numpy(), ref)
@@ -200,3 +204,60 @@ def test_iteration_gemms_on_the_emulation(dtype):
     V = vecs.cpu().numpy()[:, :nev]
     assert np.max(np.linalg.norm(H @ V - V * vals[None, :], axis=0)) <= 1e-10 * normH
     assert np.max(np.abs(V.conj().T @ V - np.eye(nev))) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["c128", "r64"])
+def test_crt_scheme_solve_and_graded_step(dtype):
+    """Ozaki scheme II (oz_crt = 1: 16 CRT moduli, exact A'B' of the 52-bit scaled operands): the
+    solve keeps the complex-double bars, and a graded H = D A D step stays at the 1e-13 bar."""
+    import paper_2205_02491_b200 as pkg
+    real = dtype == "r64"
+    N, nev, nex = 700, 40, 20
+    M = make_matrix("uniform", N, "r2" if real else "g2", seed=13)
+    H = M.dense()
+    ch = pkg.Chase(N, nev, nex, dtype=dtype)
+    ch.set_option("oz_crt", 1)
+    ch.set_option("oz_gemm_min", 0)
+    ch.set_option("oz_gemm_kmin", 0)
+    vals, vecs, rep, st = ch.solve(_dev(H), nev, nex, deg=20, tol=1e-10)
+    assert st == 0
+    normH = np.max(np.abs(M.lam))
+    assert np.max(np.abs(vals - M.lam[:nev])) <= 1e-10 * normH
+    V = vecs.cpu().numpy()[:, :nev]
+    assert np.max(np.linalg.norm(H @ V - V * vals[None, :], axis=0)) <= 1e-10 * normH
+    assert np.max(np.abs(V.conj().T @ V - np.eye(nev))) <= 1e-12
+    n = 33
+    rng = np.random.default_rng(5)
+    d = np.logspace(-6, 0, N)
+    G = (d[:, None] * H) * d[None, :]
+    X = rng.standard_normal((N, n)) + (0 if real else 1j) * rng.standard_normal((N, n))
+    ref = oracle.hemm_step(G, X, 0 * X, 0.9, 0.0, 1e-3)
+    for direction in (0, 1):
+        dY = _dev(np.zeros_like(X))
+        ch.hemm_step(direction, _dev(G), _dev(X), dY, n, 0.9, 0.0, 1e-3)
+        assert _rel(dY.cpu().numpy(), ref) <= 1e-13
+
+
+def test_crt_falls_back_to_slices_when_residues_do_not_fit(monkeypatch):
+    """oz_crt = 1 whose residue set does not fit (simulated: CHASE_OZ_CRT_MAXBYTES) continues on
+    the 7-slice scheme -- bitwise the result of a slice-scheme handle -- not on DMMA."""
+    import paper_2205_02491_b200 as pkg
+    N, n = 500, 24
+    H = make_matrix("uniform", N, "g2", seed=8).dense()
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((N, n)) + 1j * rng.standard_normal((N, n))
+    out = {}
+    for mode in ("slices", "crt-fallback", "crt"):
+        if mode == "crt-fallback":
+            monkeypatch.setenv("CHASE_OZ_CRT_MAXBYTES", "1000")
+        else:
+            monkeypatch.delenv("CHASE_OZ_CRT_MAXBYTES", raising=False)
+        ch = pkg.Chase(N, n, 1)
+        ch.set_option("oz_crt", 0 if mode == "slices" else 1)
+        dY = _dev(np.zeros((N, n), dtype=complex))
+        ch.hemm_step(0, _dev(H), _dev(X), dY, n, 1.0, 0.0, 0.0)
+        out[mode] = dY.cpu().numpy()
+        assert _rel(out[mode], H @ X) <= 1e-13, mode
+        ch.close()
+    assert np.array_equal(out["crt-fallback"], out["slices"])
+    assert not np.array_equal(out["crt"], out["slices"])     # scheme II really ran without the cap

@@ -1,6 +1,7 @@
 """Time one complex-double fused step (forward and backward) at a bench shape with the FP64 DMMA
 kernel and with the Ozaki INT8 emulation (fp64_emulation = S), and report the emulation's error
-against the DMMA result.  Usage: python tools/time_ozaki.py [N] [ncols] [S ...]"""
+against the DMMA result.  Usage: python tools/time_ozaki.py [N] [ncols] [S ...] [nodmma] [r64] [crt]
+(crt: Ozaki scheme II with 16 CRT moduli instead of S slices)"""
 import json
 import sys
 
@@ -55,6 +56,7 @@ for d in (0, 1):
     out[f"dmma_dir{d}"] = {"s": t, "tflops": fl * N * N * n / t / 1e12}
 for S in Ss:
     ch.set_option("fp64_emulation", S)
+    ch.set_option("oz_crt", 1 if "crt" in sys.argv[3:] else 0)
     for d in (0, 1):
         t, Y = run(d)
         err = (torch.linalg.norm(Y - ref[d]) / torch.linalg.norm(ref[d])).item() if d in ref else None
