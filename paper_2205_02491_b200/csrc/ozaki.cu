@@ -646,7 +646,7 @@ __global__ void oz_combine(const double* T_, int64_t ldt, int64_t tplane, const 
 
 // Scheme II reconstruction: the NMOD residues of one real product (byte planes of M x N, ld M,
 // written by the GEMM drain) -> Garner's mixed-radix digits (balanced: the representation of
-// A'B' in (-M/2, M/2), exact) -> A'B' by Horner in 128-bit integers -> one rounding to FP64 ->
+// A'B' in (-M/2, M/2), exact) -> A'B' by Horner in 64/128-bit integers -> FP64 ->
 // times 2^-104 into T (ld ldt), where oz_combine picks it up like a slice-scheme accumulator.
 __host__ __device__ constexpr int inv_mod(int a, int m) {   // a^-1 mod m (gcd(a, m) = 1)
   int t = 0, nt = 1, r = m, nr = a % m;
@@ -704,12 +704,23 @@ __global__ void __launch_bounds__(256) oz_crt(const uint8_t* C, int64_t iplane, 
 #pragma unroll
     for (int j = 0; j < NMOD; ++j) R[j] = 0;
     CrtDig<0>::run(C, iplane, idx, v, R);
-    // Horner in 128-bit integers (|A'B'| < 2^124: exact), one rounding to FP64 at the end
-    __int128 x = v[NMOD - 1];
+    // Horner in exact integers (|A'B'| < 2^124): the top 7 digits in 64 bits (|x| < 2^62), the
+    // rest in 128; then FP64 as hi 2^64 + lo (exact whenever A'B' is representable, else within
+    // one ulp -- the 128-bit software conversion costs several times more)
+    long long x64 = v[NMOD - 1];
 #pragma unroll
-    for (int j = NMOD - 2; j >= 0; --j) x = x * crt_mod(j) + v[j];
+    for (int j = NMOD - 2; j >= NMOD - 7; --j) x64 = x64 * crt_mod(j) + v[j];
+    __int128 x = x64;
+#pragma unroll
+    for (int j = NMOD - 8; j >= 0; --j) x = x * crt_mod(j) + v[j];
+    const bool neg = x < 0;
+    const unsigned __int128 ax = neg ? (unsigned __int128)(-x) : (unsigned __int128)x;   // (on the
+    const unsigned long long xh = (unsigned long long)(ax >> 64);                       // magnitude:
+    const unsigned long long xl = (unsigned long long)ax;                               // lo <= 53 bits
+    const double xa = fma((double)xh, 18446744073709551616.0, (double)xl);              // when exact)
+    const double xd = neg ? -xa : xa;
     const int m = (int)(idx % M), n = (int)(idx / M);
-    T[(int64_t)m + (int64_t)n * ldt] = (double)x * 4.930380657631324e-32;   // 2^-104
+    T[(int64_t)m + (int64_t)n * ldt] = xd * 4.930380657631324e-32;   // 2^-104
   }
 }
 
