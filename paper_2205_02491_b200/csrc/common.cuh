@@ -1,5 +1,6 @@
 // Common helpers for the ChASE B200 library (sm_100a only).
 #pragma once
+#include <unordered_map>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -44,11 +45,17 @@ __host__ __device__ inline double2 zmk(double r, double i) { return make_double2
 
 // Per-device latch for one-time kernel attribute setup (cudaFuncSetAttribute is per device, and one
 // process may drive several GPUs): true the first time it is called on the current device.
+// Per calling THREAD and device: co-located ranks are threads of one process, and a shared flag
+// would let a second thread launch before the first one's cudaFuncSetAttribute (shared-memory
+// opt-in) completed -- a failed launch on that rank and a hang on its peers.  Setting the same
+// attribute once per thread is idempotent and cheap.  `mask` only identifies the call site.
 inline bool first_on_device(unsigned long long& mask) {
   int dev = 0;
   cudaGetDevice(&dev);
+  thread_local std::unordered_map<const void*, unsigned long long> seen;
+  unsigned long long& m = seen[&mask];
   const unsigned long long bit = 1ull << (dev & 63);
-  if (mask & bit) return false;
-  mask |= bit;
+  if (m & bit) return false;
+  m |= bit;
   return true;
 }
