@@ -409,9 +409,10 @@ __host__ __device__ constexpr int crt_mod(int i) {
   return m[i];
 }
 constexpr int CRT_BITS = 52;
+constexpr double CRT_SCALE = double(1LL << CRT_BITS);            // 2^52
 
 __device__ __forceinline__ void crt_cut(double v, int8_t (&a)[NMOD]) {
-  const double A = rint(v * 4503599627370496.0);          // 2^52 v, |A| < 2^52: exact integer
+  const double A = rint(v * CRT_SCALE);                    // 2^52 v, |A| < 2^52: exact integer
 #pragma unroll
   for (int i = 0; i < NMOD; ++i) {
     const int mi = crt_mod(i);
@@ -720,7 +721,7 @@ __global__ void __launch_bounds__(256) oz_crt(const uint8_t* C, int64_t iplane, 
     const double xa = fma((double)xh, 18446744073709551616.0, (double)xl);              // when exact)
     const double xd = neg ? -xa : xa;
     const int m = (int)(idx % M), n = (int)(idx / M);
-    T[(int64_t)m + (int64_t)n * ldt] = xd * 4.930380657631324e-32;   // 2^-104
+    T[(int64_t)m + (int64_t)n * ldt] = xd * (1.0 / (CRT_SCALE * CRT_SCALE));   // 2^-104
   }
 }
 
