@@ -261,3 +261,24 @@ def test_crt_falls_back_to_slices_when_residues_do_not_fit(monkeypatch):
         ch.close()
     assert np.array_equal(out["crt-fallback"], out["slices"])
     assert not np.array_equal(out["crt"], out["slices"])     # scheme II really ran without the cap
+
+
+def test_ozaki_scheme_reported():
+    """chase_get_option("ozaki_scheme"): 2 (scheme II) by default for complex double and real, 1
+    with oz_crt = 0, 0 with the emulation off and for complex single; after a step the path that
+    ran is the one reported."""
+    import paper_2205_02491_b200 as pkg
+    N, n = 256, 8
+    H = make_matrix("uniform", N, "g2", seed=4).dense()
+    X = np.ones((N, n), dtype=complex)
+    ch = pkg.Chase(N, n, 1)
+    assert ch.get_option("ozaki_scheme") == 2
+    dY = _dev(np.zeros((N, n), dtype=complex))
+    ch.hemm_step(0, _dev(H), _dev(X), dY, n, 1.0, 0.0, 0.0)
+    assert ch.get_option("ozaki_scheme") == 2
+    ch.set_option("oz_crt", 0)
+    assert ch.get_option("ozaki_scheme") == 1 and ch.get_option("oz_crt") == 0
+    ch.set_option("fp64_emulation", 0)
+    assert ch.get_option("ozaki_scheme") == 0
+    assert pkg.Chase(N, n, 1, dtype="r64").get_option("ozaki_scheme") == 2
+    assert pkg.Chase(N, n, 1, dtype="c64").get_option("ozaki_scheme") == 0
